@@ -1,0 +1,151 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE
+(echopipe, /root/reference/pkg/src) in this container.
+
+    NUMBA_CACHE_DIR=/tmp/nb PYTHONPATH=/root/reference/pkg/src:. \
+        python tests/golden/make_golden.py
+
+/root/reference does not exist on the GPU box; the fixtures written here are
+what travels.  Inputs are NOT stored: every instance is rebuilt from a seed by
+tests/cases.py, whose draw order matches the reference's own tests.
+
+Outputs:
+  das_small.npz   criterion-4 instances (test_acceptance.py:124-177): sha256 of
+                  das_beamform output bytes for {f64, f32} x {nearest, linear},
+                  plus the full arrays of the first 12 cases.
+  chain.npz       Fig-2 chain (beamform -> analytic -> envelope -> dB, f32) on
+                  six mid-size instances: rf, envelope, display arrays and the
+                  complex analytic signal of two of them.
+  sigproc.npz     analytic_signal / dynamic_adjustment on seeded arrays.
+  configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
+                  (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
+                  N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))  # tests/
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))  # repo root
+
+import echopipe.types as ET  # noqa: E402
+from echopipe import beamform as EB  # noqa: E402
+from echopipe import environment as EE  # noqa: E402
+from echopipe import presets as EP  # noqa: E402
+from echopipe import sigproc as ES  # noqa: E402
+
+import cases  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def das_small():
+    hashes = {}
+    arrays = {}
+    for i, (ctx, data, grid, apod) in enumerate(cases.criterion4_cases(ET)):
+        for dt in ("f64", "f32"):
+            frame = ET.RfFrame(data if dt == "f64" else data.astype(np.float32))
+            for interp in ("nearest", "linear"):
+                img = EB.das_beamform(frame, ctx, grid, apod, interp=interp).data
+                hashes[f"{i}_{dt}_{interp}"] = sha(img)
+                if i < 12:
+                    arrays[f"{i}_{dt}_{interp}"] = img
+        if i < 12:
+            oracle = EB.das_beamform_oracle(ET.RfFrame(data), ctx, grid, apod, interp="linear")
+            arrays[f"{i}_f64_linear_oracle"] = oracle.data
+    keys = sorted(hashes)
+    np.savez_compressed(os.path.join(HERE, "das_small.npz"),
+                        hash_keys=np.array(keys), hash_vals=np.array([hashes[k] for k in keys]),
+                        **arrays)
+
+
+def chain():
+    arrays = {}
+    for name, ctx, data, grid, apod, interp in cases.chain_cases(ET):
+        frame = ET.RfFrame(data)
+        rf = EB.das_beamform(frame, ctx, grid, apod, interp=interp).data
+        z = ES.analytic_signal(rf, axis=0)
+        env = ES.envelope(z)
+        disp = ES.dynamic_adjustment(env, 30.0).astype(rf.dtype, copy=False)
+        arrays[f"{name}_rf"] = rf
+        arrays[f"{name}_env"] = env
+        arrays[f"{name}_disp"] = disp
+        if name in ("sta_rect_linear", "pw_t0_oddN_linear"):
+            arrays[f"{name}_z"] = z
+        # f64 chain on the same instance for the f64 GPU path
+        rf64 = EB.das_beamform(ET.RfFrame(data.astype(np.float64)), ctx, grid, apod,
+                               interp=interp).data
+        env64 = ES.envelope(ES.analytic_signal(rf64, axis=0))
+        arrays[f"{name}_rf64"] = rf64
+        arrays[f"{name}_disp64"] = ES.dynamic_adjustment(env64, 30.0)
+    np.savez_compressed(os.path.join(HERE, "chain.npz"), **arrays)
+
+
+def sigproc():
+    rng = np.random.default_rng(77)
+    out = {}
+    for n in (2, 3, 8, 9, 33, 64, 100, 256, 1000, 1024):
+        x32 = rng.normal(size=(n, 5)).astype(np.float32)
+        x64 = rng.normal(size=(n, 3))
+        out[f"x32_{n}"] = x32
+        out[f"z32_{n}"] = ES.analytic_signal(x32, axis=0)
+        out[f"x64_{n}"] = x64
+        out[f"z64_{n}"] = ES.analytic_signal(x64, axis=0)
+    e = np.abs(rng.normal(size=(64, 48))).astype(np.float32)
+    e[3, 4] = 0.0
+    out["dyn_in32"] = e
+    out["dyn_out32_30"] = ES.dynamic_adjustment(e, 30.0)
+    out["dyn_out32_45"] = ES.dynamic_adjustment(e, 45.0)
+    out["dyn_in64"] = e.astype(np.float64) * 3.0
+    out["dyn_out64_30"] = ES.dynamic_adjustment(out["dyn_in64"], 30.0)
+    np.savez_compressed(os.path.join(HERE, "sigproc.npz"), **out)
+
+
+def configs():
+    from paper_1811_01566_b200 import environment as ME
+
+    res = {}
+    specs = [("cfg1", "f32", "linear", 0), ("cfg1", "f32", "nearest", 0),
+             ("cfg1", "f64", "linear", 0), ("cfg2", "f32", "linear", 1),
+             ("cfg2", "f32", "nearest", 1), ("cfg3", "f32", "linear", 2)]
+    for name, dt, interp, seed in specs:
+        ctx_m, grid_m, n_s = ME.config_geometry(name)
+        ctx = ET.AcquisitionContext(ctx_m.speed_of_sound, ctx_m.sampling_frequency,
+                                    ctx_m.n_elements, ctx_m.pitch,
+                                    ET.PwScheme(ctx_m.tx_scheme.angles_rad) if ctx_m.is_pw
+                                    else ET.StaScheme(ctx_m.tx_scheme.tx_elements))
+        grid = ET.ImageGrid(grid_m.x_positions, grid_m.z_positions)
+        data = cases.config_rf((ctx.n_tx, ctx.n_elements, n_s), seed)
+        if dt == "f64":
+            data = data.astype(np.float64)
+        t = time.time()
+        img = EB.das_beamform(ET.RfFrame(data), ctx, grid, interp=interp).data
+        res[f"{name}_{dt}_{interp}_seed{seed}"] = sha(img)
+        print(name, dt, interp, f"{time.time() - t:.1f}s", flush=True)
+    # simulator pin: cfg2 wire phantom, f32, noise 0.01 seed 0
+    ctx_m, grid_m, n_s = ME.config_geometry("cfg2")
+    ctx = ET.AcquisitionContext(ctx_m.speed_of_sound, ctx_m.sampling_frequency,
+                                ctx_m.n_elements, ctx_m.pitch,
+                                ET.PwScheme(ctx_m.tx_scheme.angles_rad))
+    env = EE.open_simulator(EP.wire_phantom(), ctx, n_s, dtype=np.float32, seed=0,
+                            noise_std=0.01)
+    frame, _ = env.next_observation()
+    res["sim_cfg2_wire_f32_seed0_noise0.01"] = sha(frame.data)
+    with open(os.path.join(HERE, "configs.json"), "w") as f:
+        json.dump(res, f, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    for fn in (das_small, chain, sigproc, configs):
+        t = time.time()
+        fn()
+        print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)
