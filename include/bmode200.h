@@ -1,0 +1,140 @@
+/*
+ * bmode200 -- C ABI of the B200 (sm_100a) B-mode reconstruction hot path.
+ *
+ * Every entry point is stream-ordered, stateless and re-entrant: it enqueues
+ * work on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ * stream) and returns immediately.  No entry point allocates memory; all
+ * buffers are caller-owned DEVICE pointers.  Inputs are never written.
+ * Return value: BM_OK (0) or a BM_ERR_* code (see bm_error_string()).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/echopipe):
+ *   bm_das_beamform        <- _das_kernel(x_pad, tx_rows, te_idx, d_rx, weights,
+ *                             rx_map, t0_smp, half, one, nearest, uniform, out)
+ *                             beamform.py:122-187, called by das_beamform
+ *                             beamform.py:248-296 (which also builds x_pad and
+ *                             zeroes `out`, :270-274 -- both folded in here)
+ *   bm_das_aperture_span   <- _aperture_span beamform.py:66-81 (the gate half of
+ *                             aperture_weight_table :84-109, evaluated in f64)
+ *   bm_analytic_signal     <- analytic_signal sigproc.py:48-73
+ *   bm_envelope            <- envelope sigproc.py:76-78
+ *   bm_dynamic_adjustment  <- dynamic_adjustment sigproc.py:81-97
+ *   bm_envelope_peak       <- analytic_signal + envelope + the `e.max()` of
+ *                             dynamic_adjustment (sigproc.py:48-90), fused
+ *   bm_display             <- the mapping half of dynamic_adjustment
+ *                             (sigproc.py:91-97) given the peak
+ */
+#ifndef BMODE200_H
+#define BMODE200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BMODE200_ABI_VERSION 1
+
+/* element type of every floating-point buffer of one call */
+enum { BM_F32 = 0, BM_F64 = 1 };
+/* transmit scheme (types.py:62-92) */
+enum { BM_STA = 0, BM_PW = 1 };
+/* interpolation (beamform.py:43) */
+enum { BM_NEAREST = 0, BM_LINEAR = 1 };
+/* receive window (types.py:251-265) */
+enum { BM_RECTANGULAR = 0, BM_HANN = 1 };
+
+enum {
+  BM_OK = 0,
+  BM_ERR_INVALID_ARGUMENT = 1, /* a size/enum/pointer violates the contract */
+  BM_ERR_UNSUPPORTED = 2,      /* valid but outside what this build supports */
+  BM_ERR_CUDA = 3,             /* CUDA launch/runtime failure */
+  BM_ERR_AXIS_TOO_SHORT = 4    /* analytic signal axis length < 2 (sigproc.py:60-61) */
+};
+
+/*
+ * DAS geometry: the device-side form of echopipe's DasPlan (beamform.py:195-245).
+ * Instead of [n_elements, n_px] delay/weight LUTs the plan keeps only the
+ * separable inputs; the kernel rebuilds every delay with the reference's
+ * exact operation sequence, so the result is bitwise equal to das_beamform.
+ *
+ * All pointers are DEVICE pointers.
+ */
+typedef struct bm_das_geometry {
+  int32_t dtype;      /* BM_F32 | BM_F64: frame dtype, the arithmetic type   */
+  int32_t scheme;     /* BM_STA | BM_PW                                      */
+  int32_t interp;     /* BM_NEAREST | BM_LINEAR                              */
+  int32_t window;     /* BM_RECTANGULAR | BM_HANN                            */
+  int32_t uniform;    /* 1 iff rectangular and f_number == 0 (DasPlan.uniform) */
+  int32_t n_tx;       /* acquisitions                                        */
+  int32_t n_rx;       /* channels per acquisition                            */
+  int32_t n_samples;  /* samples per trace                                   */
+  int32_t n_elements; /* probe elements                                      */
+  int32_t n_z;        /* image rows (depth)                                  */
+  int32_t n_x;        /* image columns (lateral)                             */
+  int32_t reserved;
+  double speed_of_sound;     /* c  (cast to dtype, beamform.py:206)          */
+  double sampling_frequency; /* fs (cast to dtype, beamform.py:207)          */
+  const double* elem_x;      /* [n_elements] element centres, f64            */
+  const double* x_pos;       /* [n_x] grid lateral positions, f64            */
+  const double* z_pos;       /* [n_z] grid depths, f64                       */
+  const int32_t* tx_elements;/* [n_tx] STA transmit element per acquisition  */
+  const void* cos_a;         /* [n_tx] dtype, cos(angle) (PW, beamform.py:190) */
+  const void* sin_a;         /* [n_tx] dtype, sin(angle)                     */
+  const int32_t* rx_map;     /* [n_tx * n_rx] channel -> element             */
+  const void* t0_smp;        /* [n_tx] dtype, fs * t0 (beamform.py:230)      */
+  const void* hann;          /* [(n_elements + 1) * n_elements] dtype Hann table
+                                (beamform.py:48-63); NULL unless BM_HANN      */
+  const int32_t* span;       /* [2 * n_z * n_x] inclusive active span (i0, i1)
+                                per pixel, from bm_das_aperture_span; NULL
+                                when f_number == 0 (all elements active)      */
+} bm_das_geometry;
+
+/* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64
+ * (beamform.py:66-81).  span_out: device int32[2 * n_z * n_x]. */
+int bm_das_aperture_span(const bm_das_geometry* g, double f_number, int32_t* span_out,
+                         void* stream);
+
+/* Delay-and-Sum of n_frames frames.
+ *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride
+ *   out: device dtype[n_frames][n_z][n_x],  frame f at out + f*out_frame_stride
+ * Strides are in elements.  Output is fully overwritten (no pre-zeroing needed). */
+int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
+                    void* out, int64_t out_frame_stride, int32_t n_frames, void* stream);
+
+/* Analytic signal along the middle axis of a contiguous [outer, n, inner]
+ * real array x; z is complex interleaved (re, im) of the same dtype. */
+int bm_analytic_signal(int32_t dtype, const void* x, void* z, int64_t outer, int64_t n,
+                       int64_t inner, void* stream);
+
+/* e[i] = |z[i]| for `count` complex elements. */
+int bm_envelope(int32_t dtype, const void* z, void* e, int64_t count, void* stream);
+
+/* Fused analytic -> |.| -> per-frame max, along axis 0 of n_frames images
+ * [n_z, n_x] (frame f at rf_img + f*n_z*n_x).  env receives the envelope;
+ * peak receives, per frame, the max envelope as raw IEEE bits
+ * (uint32 for BM_F32, uint64 for BM_F64).  peak is reset by this call. */
+int bm_envelope_peak(int32_t dtype, const void* rf_img, void* env, void* peak,
+                     int32_t n_frames, int64_t n_z, int64_t n_x, void* stream);
+
+/* Per-frame max of `frame_elems` non-negative values (same peak encoding). */
+int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
+                  int64_t frame_elems, void* stream);
+
+/* disp = clip(20 log10(e / peak) + R, 0, R) / R, 0 where e == 0
+ * (sigproc.py:93-96), per frame; status[f] = 1 where peak <= 0 (AllZeroInput,
+ * sigproc.py:91-92), else 0.  disp has the dtype of e. */
+int bm_display(int32_t dtype, const void* e, const void* peak, void* disp, int32_t* status,
+               int32_t n_frames, int64_t frame_elems, double range_db, void* stream);
+
+/* dynamic_adjustment as one call: bm_frame_peak then bm_display. */
+int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
+                          int32_t* status, int32_t n_frames, int64_t frame_elems,
+                          double range_db, void* stream);
+
+const char* bm_error_string(int code);
+int bm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMODE200_H */

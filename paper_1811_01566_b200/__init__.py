@@ -1,0 +1,24 @@
+"""paper_1811_01566_b200 -- B200-native B-mode reconstruction hot path.
+
+Drop-in for the hot path of echopipe (the reference restatement of WaveFlow,
+arXiv 1811.01566): Delay-and-Sum for STA and plane-wave imaging, analytic-
+signal envelope detection and log compression, executed by hand-written
+sm_100a CUDA kernels in ``_lib/libbmode200.so`` (C ABI: include/bmode200.h).
+Public names mirror echopipe/__init__.py:9-64 for the path.
+"""
+
+from .beamform import INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform
+from . import engine
+from .engine import BmodeEngine
+from .environment import (Environment, Phantom, SimulatorSource, default_pw_angles,
+                          open_simulator, simulate_rf, wire_phantom)
+from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,
+                     InvalidMetadata, NativeError, NonPositiveRange, OperatorFailed, WrongStage)
+from .pipeline import (OPERATOR_REGISTRY, BenchmarkResult, OperatorKind, PipelineGraph,
+                       StageTiming, benchmark, bmode_chain, build_graph, execute,
+                       register_gpu_operators, register_operator)
+from .sigproc import analytic_signal, dynamic_adjustment, envelope
+from .types import (AcquisitionContext, ApodizationSpec, BmodeImage, ImageGrid, PwScheme,
+                    RfFrame, StaScheme, centered_rx_map, default_grid, validate_pair)
+
+__version__ = "0.1.0"

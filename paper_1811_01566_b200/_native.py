@@ -1,0 +1,107 @@
+"""ctypes binding of the bmode200 C ABI (include/bmode200.h).
+
+The library is built in-tree (``_lib/libbmode200.so``) by
+``paper_1811_01566_b200.build.build()``.  There is no CPU fallback: if the
+library or a CUDA device is missing, every op raises ``NativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libbmode200.so")
+
+BM_F32, BM_F64 = 0, 1
+BM_STA, BM_PW = 0, 1
+BM_NEAREST, BM_LINEAR = 0, 1
+BM_RECTANGULAR, BM_HANN = 0, 1
+BM_ERR_AXIS_TOO_SHORT = 4
+
+
+class DasGeometry(ctypes.Structure):
+    """Mirror of ``bm_das_geometry`` (include/bmode200.h)."""
+
+    _fields_ = [
+        ("dtype", ctypes.c_int32), ("scheme", ctypes.c_int32), ("interp", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("uniform", ctypes.c_int32), ("n_tx", ctypes.c_int32),
+        ("n_rx", ctypes.c_int32), ("n_samples", ctypes.c_int32),
+        ("n_elements", ctypes.c_int32), ("n_z", ctypes.c_int32), ("n_x", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("speed_of_sound", ctypes.c_double), ("sampling_frequency", ctypes.c_double),
+        ("elem_x", ctypes.c_void_p), ("x_pos", ctypes.c_void_p), ("z_pos", ctypes.c_void_p),
+        ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),
+        ("rx_map", ctypes.c_void_p), ("t0_smp", ctypes.c_void_p), ("hann", ctypes.c_void_p),
+        ("span", ctypes.c_void_p),
+    ]
+
+
+# every symbol declared in include/bmode200.h, with its ctypes signature
+_P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+SIGNATURES = {
+    "bm_das_aperture_span": ([ctypes.POINTER(DasGeometry), _D, _P, _P], ctypes.c_int),
+    "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
+    "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P], ctypes.c_int),
+    "bm_envelope": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
+    "bm_envelope_peak": ([_I32, _P, _P, _P, _I32, _I64, _I64, _P], ctypes.c_int),
+    "bm_frame_peak": ([_I32, _P, _P, _I32, _I64, _P], ctypes.c_int),
+    "bm_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
+    "bm_dynamic_adjustment": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
+    "bm_error_string": ([ctypes.c_int], ctypes.c_char_p),
+    "bm_abi_version": ([], ctypes.c_int),
+}
+
+_lib = None
+
+
+def load():
+    """Load the library (once) and declare every exported signature."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(-1, f"{LIB_PATH} not built; run paper_1811_01566_b200.build.build()")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib
+
+
+def check(code: int):
+    if code != 0:
+        msg = load().bm_error_string(code).decode()
+        raise NativeError(code, msg)
+
+
+def call(name: str, *args):
+    check(getattr(load(), name)(*args))
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeError(-2, "no CUDA device: the B200 path has no CPU fallback")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def dtype_code(dtype) -> int:
+    import numpy as np
+
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return BM_F32
+    if dt == np.float64:
+        return BM_F64
+    raise NativeError(1, f"unsupported dtype {dt}")

@@ -1,0 +1,204 @@
+"""Delay-and-Sum beamforming on the B200: drop-in for echopipe.beamform.
+
+Same names, parameters and defaults as the reference
+(/root/reference/pkg/src/echopipe/beamform.py):
+
+* ``DasPlan(ctx, grid, apod, dtype, n_rx)`` with ``.matches(...)``
+  (beamform.py:195-245) -- here it holds the *device* geometry (element and
+  grid positions, tx elements / PW trig, rx map, t0, Hann table, aperture
+  spans) instead of [n_elements, n_px] LUTs; the kernel rebuilds delays and
+  weights on the fly with the reference's exact rounding sequence.
+* ``das_beamform(frame, ctx, grid, apod, interp, n_threads, plan)``
+  (beamform.py:248-296) -- ``n_threads`` is accepted and ignored (the GPU
+  result is bitwise independent of any launch parameter).
+
+Output bits equal the reference's ``das_beamform`` in f32 and f64 (pinned by
+tests/test_gpu_das.py against fixtures produced by the reference).
+
+Device policy: a numpy frame is copied to the GPU and the rf image comes
+back as numpy (drop-in behaviour); a CUDA-tensor frame stays on the device
+and yields a CUDA-tensor image.  The kernel is ``bm_das_beamform`` in
+libbmode200.so; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from ._device import to_device
+from .errors import InvalidMetadata
+from .types import ApodizationSpec, BmodeImage, RfFrame, _is_torch, validate_pair
+
+INTERPOLATION_MODES = ("nearest", "linear")
+
+
+def hann_weight_table(n_elements: int) -> np.ndarray:
+    """Row M = symmetric M-point Hann window (beamform.py:48-63)."""
+    tab = np.zeros((n_elements + 1, max(n_elements, 1)))
+    for m_count in range(1, n_elements + 1):
+        if m_count == 1:
+            tab[1, 0] = 1.0
+        else:
+            k = np.arange(m_count)
+            tab[m_count, :m_count] = 0.5 - 0.5 * np.cos(2.0 * np.pi * k / (m_count - 1))
+    return tab
+
+
+def active_aperture(ctx, pixel, apod: ApodizationSpec) -> np.ndarray:
+    """Receive weight of every element for one pixel (beamform.py:84-119).
+    Host-side helper (one pixel), same f64 gate as the kernel's span."""
+    x, z = float(pixel[0]), float(pixel[1])
+    elem_x = ctx.element_positions()
+    n_el = elem_x.size
+    if apod.f_number == 0.0:
+        i0, i1 = 0, n_el - 1
+    else:
+        act = np.nonzero(np.abs(elem_x - x) <= z / (2.0 * apod.f_number))[0]
+        i0, i1 = (int(act[0]), int(act[-1])) if act.size else (0, -1)
+    w = np.zeros(n_el)
+    if i1 < i0:
+        return w
+    if apod.window == "rectangular":
+        w[i0:i1 + 1] = 1.0
+    else:
+        w[i0:i1 + 1] = hann_weight_table(n_el)[i1 - i0 + 1, : i1 - i0 + 1]
+    return w
+
+
+def _device():
+    import torch
+
+    N.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class DasPlan:
+    """Device geometry for one (ctx, grid, apod, dtype, n_rx) (beamform.py:195-245).
+
+    Immutable after construction and safe to share between threads; the
+    device buffers live on the CUDA device current at construction.
+    """
+
+    def __init__(self, ctx, grid, apod: ApodizationSpec, dtype, n_rx: int, device=None):
+        import torch
+
+        dtype = np.dtype(dtype)
+        if dtype not in (np.float32, np.float64):
+            raise InvalidMetadata("dtype", f"must be f32/f64, got {dtype}")
+        dev = torch.device(device) if device is not None else _device()
+        n_rx = int(n_rx)
+        rx_map = np.ascontiguousarray(ctx.channel_elements(n_rx), dtype=np.int32)
+        n_tx = int(ctx.n_tx)
+        t0 = np.asarray(ctx.time_zero_offset, dtype=np.float64)
+        if t0.ndim == 0:
+            t0 = np.full(n_tx, float(t0))
+        fs_t = dtype.type(ctx.sampling_frequency)
+        # host scalars computed exactly as the reference plan does (beamform.py:230, 190-192)
+        t0_smp = (fs_t * t0.astype(dtype)).astype(dtype)
+        is_pw = bool(ctx.is_pw)
+
+        def dev_t(a):
+            return to_device(a, dev)
+
+        self._bufs = {
+            "elem_x": dev_t(ctx.element_positions().astype(np.float64)),
+            "x_pos": dev_t(np.asarray(grid.x_positions, np.float64)),
+            "z_pos": dev_t(np.asarray(grid.z_positions, np.float64)),
+            "rx_map": dev_t(rx_map),
+            "t0_smp": dev_t(t0_smp),
+        }
+        if is_pw:
+            ang = np.asarray(ctx.tx_scheme.angles_rad, dtype=np.float64)
+            self._bufs["cos_a"] = dev_t(np.cos(ang).astype(dtype))
+            self._bufs["sin_a"] = dev_t(np.sin(ang).astype(dtype))
+        else:
+            self._bufs["tx_elements"] = dev_t(np.asarray(ctx.tx_scheme.tx_elements, np.int32))
+        if apod.window == "hann":
+            self._bufs["hann"] = dev_t(hann_weight_table(ctx.n_elements).astype(dtype))
+        self.uniform = apod.window == "rectangular" and apod.f_number == 0.0
+
+        g = N.DasGeometry()
+        g.dtype = N.dtype_code(dtype)
+        g.scheme = N.BM_PW if is_pw else N.BM_STA
+        g.interp = N.BM_LINEAR
+        g.window = N.BM_HANN if apod.window == "hann" else N.BM_RECTANGULAR
+        g.uniform = int(self.uniform)
+        g.n_tx, g.n_rx, g.n_samples = n_tx, n_rx, 1
+        g.n_elements, g.n_z, g.n_x = int(ctx.n_elements), int(grid.n_z), int(grid.n_x)
+        g.speed_of_sound = float(ctx.speed_of_sound)
+        g.sampling_frequency = float(ctx.sampling_frequency)
+        for name, buf in self._bufs.items():
+            setattr(g, name, buf.data_ptr())
+        if apod.f_number > 0.0:
+            span = torch.empty(2 * grid.n_z * grid.n_x, dtype=torch.int32, device=dev)
+            with torch.cuda.device(dev):
+                N.call("bm_das_aperture_span", ctypes.byref(g), float(apod.f_number),
+                       span.data_ptr(), N.stream_ptr())
+            self._bufs["span"] = span
+            g.span = span.data_ptr()
+        self._geom = g
+        self.ctx, self.grid, self.apod, self.dtype, self.n_rx = ctx, grid, apod, dtype, n_rx
+        self.device = dev
+        self.shape = (int(grid.n_z), int(grid.n_x))
+
+    def matches(self, ctx, grid, apod, dtype, n_rx) -> bool:
+        """Identity-keyed reuse test (beamform.py:238-245)."""
+        return (self.ctx is ctx and self.grid is grid and self.apod == apod
+                and self.dtype == np.dtype(dtype) and self.n_rx == n_rx)
+
+    def geometry(self, n_samples: int, interp: str) -> N.DasGeometry:
+        """A copy of the C descriptor for one launch."""
+        g = N.DasGeometry()
+        ctypes.pointer(g)[0] = self._geom
+        g.n_samples = int(n_samples)
+        g.interp = N.BM_NEAREST if interp == "nearest" else N.BM_LINEAR
+        return g
+
+    def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None):
+        """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
+        ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``."""
+        import torch
+
+        if interp not in INTERPOLATION_MODES:
+            raise InvalidMetadata("interp", f"must be one of {INTERPOLATION_MODES}")
+        single = rf.dim() == 3
+        rfb = rf.unsqueeze(0) if single else rf
+        if not rfb.is_contiguous():
+            rfb = rfb.contiguous()
+        f, n_tx, n_rx, n_s = rfb.shape
+        if rfb.dtype != (torch.float32 if self.dtype == np.float32 else torch.float64):
+            raise InvalidMetadata("data", "frame dtype differs from the plan dtype")
+        if rfb.device != self.device:
+            raise InvalidMetadata("data", f"frame on {rfb.device}, plan on {self.device}")
+        if n_tx != self._geom.n_tx or n_rx != self.n_rx:
+            raise InvalidMetadata("data", "frame shape differs from the plan")
+        if out is None:
+            out = torch.empty((f,) + self.shape, dtype=rfb.dtype, device=self.device)
+        g = self.geometry(n_s, interp)
+        n_img = self.shape[0] * self.shape[1]
+        for f0 in range(0, f, 65535):
+            nf = min(65535, f - f0)
+            N.call("bm_das_beamform", ctypes.byref(g),
+                   rfb[f0].data_ptr(), n_tx * n_rx * n_s,
+                   out[f0].data_ptr(), n_img, nf, N.stream_ptr(stream))
+        return out[0] if single else out
+
+
+def das_beamform(frame: RfFrame, ctx, grid, apod: ApodizationSpec = ApodizationSpec(),
+                 interp: str = "linear", n_threads: int | None = None,
+                 plan: DasPlan | None = None) -> BmodeImage:
+    """Delay-and-Sum the frame onto the grid; returns an rf-stage image
+    (beamform.py:248-296).  Computation runs in the frame's dtype."""
+    if interp not in INTERPOLATION_MODES:
+        raise InvalidMetadata("interp", f"must be one of {INTERPOLATION_MODES}")
+    validate_pair(frame, ctx)
+    dtype = np.dtype(frame.dtype)
+    if plan is None or not plan.matches(ctx, grid, apod, dtype, frame.n_rx):
+        plan = DasPlan(ctx, grid, apod, dtype, frame.n_rx)
+    host = not _is_torch(frame.data)
+    data = to_device(frame.data, plan.device)
+    img = plan.beamform_batch(data, interp)
+    return BmodeImage(img.cpu().numpy() if host else img, stage="rf", grid=grid)

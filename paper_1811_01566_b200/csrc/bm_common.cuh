@@ -1,0 +1,49 @@
+// Shared helpers for the bmode200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bmode200.h"
+
+namespace bm {
+
+// Exactly-rounded scalar arithmetic, one IEEE rounding per operator and no
+// FMA contraction: this is what makes the GPU delays and sums bitwise equal to
+// the reference's numpy plan + numba kernel (beamform.py:19-22, 211-216).
+template <typename T> struct R;
+template <> struct R<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+  static __device__ __forceinline__ float floor(float a) { return floorf(a); }
+  static __device__ __forceinline__ float from_double(double a) { return __double2float_rn(a); }
+};
+template <> struct R<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+  static __device__ __forceinline__ double floor(double a) { return ::floor(a); }
+  static __device__ __forceinline__ double from_double(double a) { return a; }
+};
+
+inline int cuda_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BM_OK : BM_ERR_CUDA;
+}
+
+inline int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace bm

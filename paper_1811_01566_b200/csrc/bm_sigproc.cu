@@ -1,0 +1,419 @@
+// K2: analytic signal / envelope / dynamic adjustment (sm_100a).
+//
+// Replaces sigproc.py:48-97 (analytic_signal via scipy.fft, np.abs,
+// dynamic_adjustment).  For a power-of-two lane length the whole
+//   FFT -> one-sided gain -> IFFT -> |.| -> per-frame max
+// chain runs inside one CTA's shared memory (radix-2, L lanes per CTA), so
+// the complex I/Q data never touches HBM.  Other lengths use an exact
+// O(n^2) DFT per lane (same gain convention, sigproc.py:63-70).
+#include "bm_common.cuh"
+
+namespace bm {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using type = float2; };
+template <> struct C2<double> { using type = double2; };
+
+template <typename T> struct PeakBits;
+template <> struct PeakBits<float> {
+  using U = unsigned int;
+  static __device__ __forceinline__ U bits(float v) { return __float_as_uint(v); }
+  static __device__ __forceinline__ float value(U b) { return __uint_as_float(b); }
+};
+template <> struct PeakBits<double> {
+  using U = unsigned long long;
+  static __device__ __forceinline__ U bits(double v) { return (U)__double_as_longlong(v); }
+  static __device__ __forceinline__ double value(U b) { return __longlong_as_double((long long)b); }
+};
+
+// sigproc.py:63-70
+template <typename T>
+__device__ __forceinline__ T hilbert_gain(int64_t k, int64_t n) {
+  if (k == 0) return T(1);
+  if ((n & 1) == 0) {
+    if (k == n / 2) return T(1);
+    return k < n / 2 ? T(2) : T(0);
+  }
+  return k <= (n - 1) / 2 ? T(2) : T(0);
+}
+
+template <typename T>
+__device__ __forceinline__ typename C2<T>::type cmul(typename C2<T>::type a,
+                                                     typename C2<T>::type b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+
+template <typename T>
+__device__ __forceinline__ T magnitude(T re, T im) {
+  return hypot(re, im);
+}
+
+template <typename T>
+__device__ __forceinline__ void block_peak(T v, typename PeakBits<T>::U* peak) {
+  // warp max then one atomic per warp (values are >= 0, so IEEE bits order
+  // like the values)
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(peak, PeakBits<T>::bits(v));
+}
+
+enum OutMode { kComplex = 0, kEnvelope = 1 };
+
+// Power-of-two lanes: L lanes of length n per CTA, radix-2 DIT in shared memory.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict__ x, T* __restrict__ out,
+                                                            typename PeakBits<T>::U* __restrict__ peak,
+                                                            int64_t n, int log2n, int64_t inner,
+                                                            int L) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* tw = reinterpret_cast<V*>(smem_raw);  // [n/2]
+  V* buf = tw + n / 2;                       // [L][n]
+  const int64_t o = blockIdx.y;
+  const int64_t i_base = (int64_t)blockIdx.x * L;
+  const int lanes = (int)((inner - i_base) < L ? (inner - i_base) : L);
+  const int64_t half_n = n >> 1;
+
+  for (int64_t k = threadIdx.x; k < half_n; k += blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)n, &s, &c);
+    tw[k] = V{(T)c, (T)s};
+  }
+  const T* xo = x + o * n * inner + i_base;
+  for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
+    const int64_t k = idx / lanes;
+    const int l = (int)(idx % lanes);
+    const int64_t r = __brevll((unsigned long long)k) >> (64 - log2n);
+    buf[l * n + r] = V{xo[k * inner + l], T(0)};
+  }
+  __syncthreads();
+
+  for (int pass = 0; pass < 2; ++pass) {
+    const T sign = pass == 0 ? T(1) : T(-1);  // inverse: conjugate twiddles
+    for (int s = 1; s <= log2n; ++s) {
+      const int64_t h = (int64_t)1 << (s - 1);
+      for (int64_t b = threadIdx.x; b < half_n * lanes; b += blockDim.x) {
+        const int l = (int)(b / half_n);
+        const int64_t bb = b % half_n;
+        const int64_t pos = bb & (h - 1);
+        const int64_t i = ((bb >> (s - 1)) << s) + pos;
+        V w = tw[pos << (log2n - s)];
+        w.y *= sign;
+        V* lane = buf + l * n;
+        const V u = lane[i];
+        const V t = cmul<T>(w, lane[i + h]);
+        lane[i] = V{u.x + t.x, u.y + t.y};
+        lane[i + h] = V{u.x - t.x, u.y - t.y};
+      }
+      __syncthreads();
+    }
+    if (pass == 0) {
+      // one-sided gain, then bit-reverse permutation for the inverse DIT
+      for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
+        const int l = (int)(idx / n);
+        const int64_t k = idx % n;
+        const int64_t r = __brevll((unsigned long long)k) >> (64 - log2n);
+        if (k > r) continue;
+        V* lane = buf + l * n;
+        const T gk = hilbert_gain<T>(k, n), gr = hilbert_gain<T>(r, n);
+        const V a = lane[k], bv = lane[r];
+        lane[k] = V{bv.x * gr, bv.y * gr};
+        lane[r] = V{a.x * gk, a.y * gk};
+      }
+      __syncthreads();
+    }
+  }
+
+  const T inv_n = T(1) / T(n);
+  T vmax = T(0);
+  for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
+    const int64_t k = idx / lanes;
+    const int l = (int)(idx % lanes);
+    const V z = buf[l * n + k];
+    const T re = z.x * inv_n, im = z.y * inv_n;
+    const int64_t g = o * n * inner + k * inner + i_base + l;
+    if (MODE == kComplex) {
+      reinterpret_cast<V*>(out)[g] = V{re, im};
+    } else {
+      const T e = magnitude(re, im);
+      out[g] = e;
+      vmax = e > vmax ? e : vmax;
+    }
+  }
+  if (MODE == kEnvelope) block_peak<T>(vmax, peak + o);
+}
+
+// General n: exact DFT per lane (one lane per CTA).  Positive-frequency bins
+// only (the gain zeroes the rest), twiddles from an exact (j*k mod n) table.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) analytic_dft_kernel(const T* __restrict__ x, T* __restrict__ out,
+                                                           typename PeakBits<T>::U* __restrict__ peak,
+                                                           int64_t n, int64_t inner) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* tw = reinterpret_cast<V*>(smem_raw);  // [n]
+  const int64_t nb = n / 2 + 1;           // bins 0..n/2
+  V* X = tw + n;                           // [nb]
+  T* xs = reinterpret_cast<T*>(X + nb);    // [n]
+  const int64_t o = blockIdx.y, i = blockIdx.x;
+  const int64_t base = o * n * inner + i;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)n, &s, &c);
+    tw[k] = V{(T)c, (T)s};
+    xs[k] = x[base + k * inner];
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < nb; k += blockDim.x) {
+    T re = 0, im = 0;
+    int64_t r = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      const V w = tw[r];
+      re += xs[j] * w.x;
+      im += xs[j] * w.y;
+      r += k;
+      if (r >= n) r -= n;
+    }
+    const T g = hilbert_gain<T>(k, n);
+    X[k] = V{re * g, im * g};
+  }
+  __syncthreads();
+  const T inv_n = T(1) / T(n);
+  T vmax = T(0);
+  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    T re = 0, im = 0;
+    int64_t r = 0;
+    for (int64_t k = 0; k < nb; ++k) {
+      const V w = tw[r];  // exp(-2 pi i k t / n); inverse uses the conjugate
+      const V a = X[k];
+      re += a.x * w.x + a.y * w.y;
+      im += a.y * w.x - a.x * w.y;
+      r += t;
+      if (r >= n) r -= n;
+    }
+    re *= inv_n;
+    im *= inv_n;
+    if (MODE == kComplex) {
+      reinterpret_cast<V*>(out)[base + t * inner] = V{re, im};
+    } else {
+      const T e = magnitude(re, im);
+      out[base + t * inner] = e;
+      vmax = e > vmax ? e : vmax;
+    }
+  }
+  if (MODE == kEnvelope) block_peak<T>(vmax, peak + o);
+}
+
+template <typename T>
+__global__ void envelope_kernel(const T* __restrict__ z, T* __restrict__ e, int64_t count) {
+  using V = typename C2<T>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const V v = reinterpret_cast<const V*>(z)[i];
+    e[i] = magnitude(v.x, v.y);
+  }
+}
+
+template <typename T>
+__global__ void peak_kernel(const T* __restrict__ e, typename PeakBits<T>::U* __restrict__ peak,
+                            int64_t frame_elems) {
+  const int64_t f = blockIdx.y;
+  const T* ef = e + f * frame_elems;
+  T vmax = T(0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = ef[i];
+    vmax = v > vmax ? v : vmax;
+  }
+  block_peak<T>(vmax, peak + f);
+}
+
+template <typename T>
+__device__ __forceinline__ T log10_rn(T v);
+template <>
+__device__ __forceinline__ float log10_rn<float>(float v) {
+  return __double2float_rn(log10((double)v));
+}
+template <>
+__device__ __forceinline__ double log10_rn<double>(double v) {
+  return log10(v);
+}
+
+// sigproc.py:90-96, in the input precision: q = e/peak; db = 20*log10(q);
+// out = clip(db + R, 0, R) / R; zeros map to 0 without the log.
+template <typename T>
+__global__ void display_kernel(const T* __restrict__ e, const typename PeakBits<T>::U* __restrict__ peak,
+                               T* __restrict__ disp, int32_t* __restrict__ status,
+                               int64_t frame_elems, double range_db) {
+  using O = R<T>;
+  const int64_t f = blockIdx.y;
+  const T pk = PeakBits<T>::value(peak[f]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && status) status[f] = pk > T(0) ? 0 : 1;
+  const T r = O::from_double(range_db);
+  const T* ef = e + f * frame_elems;
+  T* df = disp + f * frame_elems;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = ef[i];
+    T outv = T(0);
+    if (v > T(0) && pk > T(0)) {
+      const T db = O::mul(T(20), log10_rn<T>(O::div(v, pk)));
+      T s = O::add(db, r);
+      s = s < T(0) ? T(0) : (s > r ? r : s);
+      outv = O::div(s, r);
+    }
+    df[i] = outv;
+  }
+}
+
+static inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+static inline int ilog2(int64_t n) {
+  int l = 0;
+  while (((int64_t)1 << l) < n) ++l;
+  return l;
+}
+
+template <typename T, int MODE>
+static int launch_analytic(const T* x, T* out, typename PeakBits<T>::U* peak, int64_t outer,
+                           int64_t n, int64_t inner, cudaStream_t s) {
+  using V = typename C2<T>::type;
+  if (outer > 65535) return BM_ERR_UNSUPPORTED;
+  if (is_pow2(n)) {
+    const size_t lane_bytes = (size_t)n * sizeof(V);
+    const size_t tw_bytes = (size_t)(n / 2) * sizeof(V);
+    int L = (int)((96 * 1024) / lane_bytes);
+    L = L < 1 ? 1 : (L > 16 ? 16 : L);
+    if (L > inner) L = (int)inner;
+    const size_t smem = tw_bytes + L * lane_bytes;
+    if (smem > 220 * 1024) return BM_ERR_UNSUPPORTED;
+    auto k = analytic_pow2_kernel<T, MODE>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return BM_ERR_CUDA;
+    dim3 grid((unsigned)((inner + L - 1) / L), (unsigned)outer);
+    k<<<grid, 256, smem, s>>>(x, out, peak, n, ilog2(n), inner, L);
+  } else {
+    const size_t smem = (size_t)n * sizeof(V) + (size_t)(n / 2 + 1) * sizeof(V) + (size_t)n * sizeof(T);
+    if (smem > 220 * 1024 || inner > 0x7fffffff) return BM_ERR_UNSUPPORTED;
+    auto k = analytic_dft_kernel<T, MODE>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return BM_ERR_CUDA;
+    dim3 grid((unsigned)inner, (unsigned)outer);
+    k<<<grid, 256, smem, s>>>(x, out, peak, n, inner);
+  }
+  return cuda_status();
+}
+
+static inline int grid_for(int64_t count) {
+  int64_t b = (count + 255) / 256;
+  const int64_t cap = 8LL * sm_count();
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int bm_analytic_signal(int32_t dtype, const void* x, void* z, int64_t outer, int64_t n,
+                                  int64_t inner, void* stream) {
+  if (!x || !z || outer < 1 || inner < 1) return BM_ERR_INVALID_ARGUMENT;
+  if (n < 2) return BM_ERR_AXIS_TOO_SHORT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == BM_F32)
+    return launch_analytic<float, kComplex>((const float*)x, (float*)z, nullptr, outer, n, inner, s);
+  if (dtype == BM_F64)
+    return launch_analytic<double, kComplex>((const double*)x, (double*)z, nullptr, outer, n, inner, s);
+  return BM_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int bm_envelope(int32_t dtype, const void* z, void* e, int64_t count, void* stream) {
+  if (!z || !e || count < 0) return BM_ERR_INVALID_ARGUMENT;
+  if (count == 0) return BM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == BM_F32)
+    envelope_kernel<float><<<grid_for(count), 256, 0, s>>>((const float*)z, (float*)e, count);
+  else if (dtype == BM_F64)
+    envelope_kernel<double><<<grid_for(count), 256, 0, s>>>((const double*)z, (double*)e, count);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}
+
+extern "C" int bm_envelope_peak(int32_t dtype, const void* rf_img, void* env, void* peak,
+                                int32_t n_frames, int64_t n_z, int64_t n_x, void* stream) {
+  if (!rf_img || !env || !peak || n_frames < 1 || n_x < 1) return BM_ERR_INVALID_ARGUMENT;
+  if (n_z < 2) return BM_ERR_AXIS_TOO_SHORT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t pb = dtype == BM_F64 ? 8 : 4;
+  if (cudaMemsetAsync(peak, 0, pb * n_frames, s) != cudaSuccess) return BM_ERR_CUDA;
+  if (dtype == BM_F32)
+    return launch_analytic<float, kEnvelope>((const float*)rf_img, (float*)env,
+                                             (unsigned int*)peak, n_frames, n_z, n_x, s);
+  if (dtype == BM_F64)
+    return launch_analytic<double, kEnvelope>((const double*)rf_img, (double*)env,
+                                              (unsigned long long*)peak, n_frames, n_z, n_x, s);
+  return BM_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
+                             int64_t frame_elems, void* stream) {
+  if (!e || !peak || n_frames < 1 || n_frames > 65535 || frame_elems < 0)
+    return BM_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t pb = dtype == BM_F64 ? 8 : 4;
+  if (cudaMemsetAsync(peak, 0, pb * n_frames, s) != cudaSuccess) return BM_ERR_CUDA;
+  if (frame_elems == 0) return BM_OK;
+  int gx = grid_for(frame_elems);
+  if (gx > 2 * sm_count()) gx = 2 * sm_count();
+  dim3 grid(gx, n_frames);
+  if (dtype == BM_F32)
+    peak_kernel<float><<<grid, 256, 0, s>>>((const float*)e, (unsigned int*)peak, frame_elems);
+  else if (dtype == BM_F64)
+    peak_kernel<double><<<grid, 256, 0, s>>>((const double*)e, (unsigned long long*)peak, frame_elems);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}
+
+extern "C" int bm_display(int32_t dtype, const void* e, const void* peak, void* disp,
+                          int32_t* status, int32_t n_frames, int64_t frame_elems, double range_db,
+                          void* stream) {
+  if (!e || !peak || !disp || n_frames < 1 || n_frames > 65535 || frame_elems < 0)
+    return BM_ERR_INVALID_ARGUMENT;
+  if (!(range_db > 0) || range_db != range_db) return BM_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int gx = grid_for(frame_elems);
+  if (gx > 2 * sm_count()) gx = 2 * sm_count();
+  dim3 grid(gx, n_frames);
+  if (dtype == BM_F32)
+    display_kernel<float><<<grid, 256, 0, s>>>((const float*)e, (const unsigned int*)peak,
+                                              (float*)disp, status, frame_elems, range_db);
+  else if (dtype == BM_F64)
+    display_kernel<double><<<grid, 256, 0, s>>>((const double*)e, (const unsigned long long*)peak,
+                                               (double*)disp, status, frame_elems, range_db);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}
+
+extern "C" int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
+                                     int32_t* status, int32_t n_frames, int64_t frame_elems,
+                                     double range_db, void* stream) {
+  int rc = bm_frame_peak(dtype, e, peak_ws, n_frames, frame_elems, stream);
+  if (rc) return rc;
+  return bm_display(dtype, e, peak_ws, disp, status, n_frames, frame_elems, range_db, stream);
+}
+
+extern "C" const char* bm_error_string(int code) {
+  switch (code) {
+    case BM_OK: return "ok";
+    case BM_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case BM_ERR_UNSUPPORTED: return "unsupported size for this build";
+    case BM_ERR_CUDA: return "CUDA runtime error";
+    case BM_ERR_AXIS_TOO_SHORT: return "analytic signal needs axis length >= 2";
+    default: return "unknown error";
+  }
+}
+
+extern "C" int bm_abi_version(void) { return BMODE200_ABI_VERSION; }

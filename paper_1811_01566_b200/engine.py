@@ -1,0 +1,170 @@
+"""Batched B-mode reconstruction engine (cine streams).
+
+The reference reconstructs one observation at a time through its graph
+executor (pipeline.py:355-437, driven per frame by ``benchmark``).  For
+streams of frames that share one acquisition geometry -- BASELINE config 4,
+"batched cine stream" -- this engine runs the same chain
+
+    das_beamform -> analytic_signal -> envelope -> dynamic_adjustment
+
+on a batch of frames with three launches (``bm_das_beamform``,
+``bm_envelope_peak``, ``bm_display``) and, for host-resident input, overlaps
+the host->device copy of chunk i+1 and the device->host copy of chunk i-1
+with the reconstruction of chunk i (SURVEY §8(f) "next #1": RF ingest).
+
+Results are identical to running ``bmode_chain`` per frame: every kernel is
+per-frame independent (DAS bitwise equal to the reference; peak per frame).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .beamform import DasPlan
+from .errors import AllZeroInput, InvalidMetadata, NonPositiveRange
+from .types import ApodizationSpec
+
+
+class BmodeEngine:
+    """Reconstruct batches of frames of one (ctx, grid) on one GPU."""
+
+    def __init__(self, ctx, grid, apod: ApodizationSpec = ApodizationSpec(),
+                 interp: str = "linear", range_db: float = 30.0, dtype=np.float32,
+                 n_rx: int | None = None, device=None):
+        import torch
+
+        if not (np.isfinite(range_db) and range_db > 0):
+            raise NonPositiveRange(f"range_db must be > 0, got {range_db}")
+        if interp not in ("nearest", "linear"):
+            raise InvalidMetadata("interp", "must be one of ('nearest', 'linear')")
+        n_rx = int(n_rx if n_rx is not None else (
+            ctx.rx_channel_map.shape[1] if ctx.rx_channel_map is not None else ctx.n_elements))
+        self.plan = DasPlan(ctx, grid, apod, dtype, n_rx, device=device)
+        self.device = self.plan.device
+        self.dtype = np.dtype(dtype)
+        self.tdtype = torch.float32 if self.dtype == np.float32 else torch.float64
+        self.code = N.dtype_code(self.dtype)
+        self.interp = interp
+        self.range_db = float(range_db)
+        self.frame_shape = (int(ctx.n_tx), n_rx)
+        self.image_shape = self.plan.shape
+        self._ws = {}
+        self.launches = 0
+
+    # ------------------------------------------------------------------ device
+    def _buffers(self, n_frames: int, key="dev"):
+        import torch
+
+        cur = self._ws.get(key)
+        if cur is None or cur[0] < n_frames:
+            nz, nx = self.image_shape
+            rf_img = torch.empty((n_frames, nz, nx), dtype=self.tdtype, device=self.device)
+            env = torch.empty_like(rf_img)
+            peak = torch.empty(n_frames, dtype=torch.int32 if self.code == N.BM_F32 else torch.int64,
+                               device=self.device)
+            status = torch.zeros(n_frames, dtype=torch.int32, device=self.device)
+            cur = (n_frames, rf_img, env, peak, status)
+            self._ws[key] = cur
+        return cur
+
+    def reconstruct(self, rf, out=None, stream=None, key="dev", status=None, das_events=None):
+        """Device batch ``rf [F, n_tx, n_rx, n_s]`` -> display ``[F, n_z, n_x]``
+        (enqueued on ``stream``; no synchronisation).  Per-frame all-zero
+        status is kept for :meth:`check`."""
+        import torch
+
+        f = int(rf.shape[0])
+        _, rf_img, env, peak, st = self._buffers(f, key)
+        rf_img, env, peak = rf_img[:f], env[:f], peak[:f]
+        status = st[:f] if status is None else status
+        if out is None:
+            out = torch.empty((f,) + self.image_shape, dtype=self.tdtype, device=self.device)
+        s = N.stream_ptr(stream)
+        if das_events is not None:
+            das_events[0].record(stream)
+        self.plan.beamform_batch(rf, self.interp, out=rf_img, stream=stream)
+        if das_events is not None:
+            das_events[1].record(stream)
+        nz, nx = self.image_shape
+        N.call("bm_envelope_peak", self.code, rf_img.data_ptr(), env.data_ptr(), peak.data_ptr(),
+               f, nz, nx, s)
+        N.call("bm_display", self.code, env.data_ptr(), peak.data_ptr(), out.data_ptr(),
+               status.data_ptr(), f, nz * nx, self.range_db, s)
+        self.launches += 3
+        if not isinstance(key, tuple):
+            self._last_status = status
+        return out
+
+    def check(self):
+        """Raise AllZeroInput if any frame of the last batch had no positive
+        envelope sample (synchronises)."""
+        st = getattr(self, "_last_status", None)
+        if st is not None and int(st.max().item()) != 0:
+            raise AllZeroInput("dynamic adjustment needs a strictly positive element")
+
+    # -------------------------------------------------------------------- host
+    def pinned(self, n_frames: int, n_samples: int):
+        """Pinned host buffers for a host-streamed batch: (rf_host, disp_host)."""
+        import torch
+
+        rf = torch.empty((n_frames,) + self.frame_shape + (n_samples,), dtype=self.tdtype,
+                         pin_memory=True)
+        disp = torch.empty((n_frames,) + self.image_shape, dtype=self.tdtype, pin_memory=True)
+        return rf, disp
+
+    def reconstruct_host(self, rf_host, disp_host=None, chunk: int = 4):
+        """Host batch -> host display with copy/compute overlap.
+
+        ``rf_host`` should be pinned (see :meth:`pinned`) for the copies to be
+        asynchronous.  Chunk i+1 is uploaded on an H2D stream and chunk i-1
+        downloaded on a D2H stream while chunk i is reconstructed on the
+        current stream.  Returns ``disp_host`` after synchronising."""
+        import torch
+
+        f = int(rf_host.shape[0])
+        if disp_host is None:
+            disp_host = torch.empty((f,) + self.image_shape, dtype=self.tdtype,
+                                    pin_memory=True)
+        chunk = max(1, min(chunk, f))
+        n_s = int(rf_host.shape[-1])
+        key = ("host", chunk, n_s)
+        if key not in self._ws:
+            bufs = [torch.empty((chunk,) + self.frame_shape + (n_s,), dtype=self.tdtype,
+                                device=self.device) for _ in range(2)]
+            outs = [torch.empty((chunk,) + self.image_shape, dtype=self.tdtype,
+                                device=self.device) for _ in range(2)]
+            self._ws[key] = (bufs, outs, torch.cuda.Stream(self.device),
+                             torch.cuda.Stream(self.device))
+        bufs, outs, h2d, d2h = self._ws[key]
+        comp = torch.cuda.current_stream(self.device)
+        n_chunks = (f + chunk - 1) // chunk
+        up_done = [None, None]
+        comp_done = [None, None]
+        down_done = [None, None]
+        status = torch.zeros(f, dtype=torch.int32, device=self.device)
+        self._last_status = status
+        for i in range(n_chunks):
+            slot = i % 2
+            lo, hi = i * chunk, min(f, (i + 1) * chunk)
+            with torch.cuda.stream(h2d):
+                if comp_done[slot] is not None:
+                    h2d.wait_event(comp_done[slot])  # slot's rf buffer free again
+                bufs[slot][: hi - lo].copy_(rf_host[lo:hi], non_blocking=True)
+                up_done[slot] = torch.cuda.Event()
+                up_done[slot].record(h2d)
+            comp.wait_event(up_done[slot])
+            if down_done[slot] is not None:
+                comp.wait_event(down_done[slot])  # slot's output buffer drained
+            self.reconstruct(bufs[slot][: hi - lo], out=outs[slot][: hi - lo], stream=comp,
+                             key=("host", chunk), status=status[lo:hi])
+            comp_done[slot] = torch.cuda.Event()
+            comp_done[slot].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(comp_done[slot])
+                disp_host[lo:hi].copy_(outs[slot][: hi - lo], non_blocking=True)
+                down_done[slot] = torch.cuda.Event()
+                down_done[slot].record(d2h)
+        d2h.synchronize()
+        comp.synchronize()
+        return disp_host

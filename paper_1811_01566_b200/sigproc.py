@@ -1,0 +1,139 @@
+"""Envelope detection and log compression on the B200: drop-in for the hot
+half of echopipe.sigproc (/root/reference/pkg/src/echopipe/sigproc.py:48-97).
+
+* ``analytic_signal(x, axis=-1)``  -- sigproc.py:48-73 (one-sided spectrum
+  doubling, same gain convention for even/odd N); complex64 for f32 input,
+  complex128 otherwise, as scipy.fft returns.
+* ``envelope(z)``                   -- sigproc.py:76-78.
+* ``dynamic_adjustment(e, range_db)`` -- sigproc.py:81-97; returns float64
+  like the reference (values computed in the input precision).
+
+Device policy as in beamform.py: numpy in -> numpy out; CUDA tensor in ->
+CUDA tensor out.  Kernels: ``bm_analytic_signal``, ``bm_envelope``,
+``bm_dynamic_adjustment`` (libbmode200.so).  Errors are raised before any
+launch, with the reference's exception types; AllZeroInput needs the
+device-side peak and is raised after one synchronisation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from ._device import to_device
+from .errors import AllZeroInput, AxisTooShort, NonPositiveRange
+from .types import _is_torch, _np_dtype
+
+
+def _dev():
+    import torch
+
+    N.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _real_dtype_for(a):
+    dt = np.dtype(_np_dtype(a))
+    if np.issubdtype(dt, np.complexfloating):
+        raise ValueError("analytic_signal expects a real tensor")
+    return np.dtype(np.float32) if dt in (np.float32, np.float16) else np.dtype(np.float64)
+
+
+def analytic_signal(x, axis: int = -1):
+    """Analytic signal of a real tensor via one-sided spectrum doubling."""
+    import torch
+
+    is_t = _is_torch(x)
+    if not is_t:
+        x = np.asarray(x)
+    rdt = _real_dtype_for(x)
+    n = int(x.shape[axis])
+    if n < 2:
+        raise AxisTooShort("analytic signal needs axis length >= 2")
+    dev = x.device if is_t and x.is_cuda else _dev()
+    tdt = torch.float32 if rdt == np.float32 else torch.float64
+    xd = to_device(x, dev, tdt)
+    ax = axis % xd.dim()
+    shape = tuple(xd.shape)
+    outer = int(np.prod(shape[:ax], dtype=np.int64))
+    inner = int(np.prod(shape[ax + 1:], dtype=np.int64))
+    z = torch.empty(shape + (2,), dtype=tdt, device=dev)
+    if xd.numel():
+        with torch.cuda.device(dev):
+            for o0 in range(0, outer, 65535):
+                no = min(65535, outer - o0)
+                N.call("bm_analytic_signal", N.dtype_code(rdt), xd.reshape(-1)[o0 * n * inner:].data_ptr(),
+                       z.reshape(-1)[o0 * n * inner * 2:].data_ptr(), no, n, inner, N.stream_ptr())
+    zc = torch.view_as_complex(z)
+    if is_t and x.is_cuda:
+        return zc
+    return zc.cpu().numpy()
+
+
+def envelope(z):
+    """Elementwise magnitude |z| (sigproc.py:76-78)."""
+    import torch
+
+    is_t = _is_torch(z)
+    if not is_t:
+        z = np.asarray(z)
+        if not np.iscomplexobj(z):
+            return np.abs(z)
+    elif not z.is_complex():
+        return z.abs()
+    dev = z.device if is_t and z.is_cuda else _dev()
+    zd = to_device(z, dev)
+    rdt = torch.float32 if zd.dtype == torch.complex64 else torch.float64
+    if zd.dtype not in (torch.complex64, torch.complex128):
+        zd = zd.to(torch.complex128)
+    zr = torch.view_as_real(zd.contiguous())
+    e = torch.empty(zd.shape, dtype=rdt, device=dev)
+    with torch.cuda.device(dev):
+        N.call("bm_envelope", N.BM_F32 if rdt == torch.float32 else N.BM_F64, zr.data_ptr(),
+               e.data_ptr(), zd.numel(), N.stream_ptr())
+    return e if is_t and z.is_cuda else e.cpu().numpy()
+
+
+def _dyn_device(e, range_db: float, peak=None):
+    """dB mapping on the device in e's precision; returns (disp, status)."""
+    import torch
+
+    dev = e.device
+    code = N.BM_F32 if e.dtype == torch.float32 else N.BM_F64
+    disp = torch.empty_like(e)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        if peak is None:
+            peak = torch.empty(1, dtype=torch.int32 if code == N.BM_F32 else torch.int64, device=dev)
+            N.call("bm_dynamic_adjustment", code, e.data_ptr(), peak.data_ptr(), disp.data_ptr(),
+                   status.data_ptr(), 1, e.numel(), float(range_db), N.stream_ptr())
+        else:
+            N.call("bm_display", code, e.data_ptr(), peak.data_ptr(), disp.data_ptr(),
+                   status.data_ptr(), 1, e.numel(), float(range_db), N.stream_ptr())
+    return disp, status
+
+
+def dynamic_adjustment(e, range_db: float):
+    """Log-compress an envelope to display values in [0, 1] (sigproc.py:81-97).
+
+    The per-frame peak maps to 1; anything ``range_db`` or more below the
+    peak maps to 0; zero inputs map to 0.  Returns float64 like the reference.
+    """
+    import torch
+
+    if not (np.isfinite(range_db) and range_db > 0):
+        raise NonPositiveRange(f"range_db must be > 0, got {range_db}")
+    is_t = _is_torch(e)
+    if not is_t:
+        e = np.asarray(e)
+    if (e.numel() if is_t else e.size) == 0:
+        raise AllZeroInput("dynamic adjustment needs a strictly positive element")
+    dt = np.dtype(_np_dtype(e))
+    rdt = torch.float32 if dt == np.float32 else torch.float64
+    dev = e.device if is_t and e.is_cuda else _dev()
+    ed = to_device(e, dev, rdt)
+    disp, status = _dyn_device(ed.reshape(-1), range_db)
+    if int(status.item()) != 0:
+        raise AllZeroInput("dynamic adjustment needs a strictly positive element")
+    out = disp.reshape(ed.shape).to(torch.float64)
+    return out if is_t and e.is_cuda else out.cpu().numpy()

@@ -1,0 +1,100 @@
+"""GPU: the full Fig-2 chain through the operator registry (bmode_chain ->
+build_graph -> execute) against the reference's chain outputs, and the
+reference's pipeline-level behaviours (test_pipeline.py / test_acceptance.py)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import cases
+import paper_1811_01566_b200 as bm
+from paper_1811_01566_b200.errors import OperatorFailed
+
+pytestmark = pytest.mark.gpu
+
+# f32 chain tolerances vs the reference (DAS is bitwise; FFT is not):
+ENV_REL = 2e-6   # max|d env| / max env
+DISP_ABS = 2e-5  # display units ([0, 1]); ~6e-4 dB of a 30 dB range
+
+
+def run_chain(ctx, data, grid, apod, interp):
+    spec = bm.bmode_chain(window=apod.window, f_number=apod.f_number, interpolation=interp,
+                          grid={"x_positions": grid.x_positions.tolist(),
+                                "z_positions": grid.z_positions.tolist()})
+    spec["outputs"] = ["beamform", "envelope", "dynamic_adjustment"]
+    graph = bm.build_graph(spec)
+    outs, timing = bm.execute(graph, (bm.RfFrame(data), ctx))
+    return outs, timing
+
+
+def test_chain_vs_reference(golden_dir):
+    g = np.load(os.path.join(golden_dir, "chain.npz"))
+    for name, ctx, data, grid, apod, interp in cases.chain_cases(bm.types):
+        outs, timing = run_chain(ctx, data, grid, apod, interp)
+        rf = outs["beamform"].numpy()
+        env = outs["envelope"].numpy()
+        disp = outs["dynamic_adjustment"].numpy()
+        assert rf.tobytes() == g[f"{name}_rf"].tobytes(), name
+        ref_env = g[f"{name}_env"]
+        assert np.abs(env - ref_env).max() <= ENV_REL * ref_env.max(), name
+        assert disp.dtype == np.float32
+        assert np.abs(disp - g[f"{name}_disp"]).max() <= DISP_ABS, name
+        assert disp.max() == 1.0 and disp.min() >= 0.0
+        assert [s for s, _ in timing.stages] == ["beamform", "analytic_signal", "envelope",
+                                                 "dynamic_adjustment"]
+        assert all(ms >= 0 for _, ms in timing.stages)
+
+
+def test_deferred_analytic_materialises(golden_dir):
+    g = np.load(os.path.join(golden_dir, "chain.npz"))
+    name, ctx, data, grid, apod, interp = cases.chain_cases(bm.types)[0]
+    spec = bm.bmode_chain(grid={"x_positions": grid.x_positions.tolist(),
+                                "z_positions": grid.z_positions.tolist()})
+    spec["outputs"] = ["analytic_signal", "dynamic_adjustment"]
+    outs, _ = bm.execute(bm.build_graph(spec), (bm.RfFrame(data), ctx))
+    z = outs["analytic_signal"].data.cpu().numpy()
+    ref = g[f"{name}_z"]
+    assert np.abs(z - ref).max() <= 2e-6 * np.abs(ref).max()
+
+
+def test_all_zero_frame_fails_in_dynamic_adjustment():
+    ctx = bm.AcquisitionContext(1540.0, 40e6, 8, 2e-4, bm.StaScheme(tuple(range(8))))
+    graph = bm.build_graph(bm.bmode_chain())
+    with pytest.raises(OperatorFailed) as err:
+        bm.execute(graph, (bm.RfFrame(np.zeros((8, 8, 256))), ctx))
+    assert err.value.node == "dynamic_adjustment"
+
+
+def test_localization_sta_and_pw():
+    """Criterion 3 (test_acceptance.py:90-121): the envelope argmax of a
+    simulated point scatterer lands within +/-1 cell for STA and PW."""
+    scat = (0.45e-3, 14.2e-3)
+    ph = bm.Phantom(((scat[0], scat[1], 1.0),), center_frequency=5e6, n_cycles=2)
+    for scheme in ("sta", "pw"):
+        tx = (bm.StaScheme(tuple(range(32))) if scheme == "sta"
+              else bm.PwScheme(tuple(bm.default_pw_angles())))
+        ctx = bm.AcquisitionContext(1540.0, 40e6, 32, 2e-4, tx)
+        frame = bm.simulate_rf(ph, ctx, 1024)
+        grid = bm.default_grid(ctx, 1024, scheme)
+        img = bm.das_beamform(frame, ctx, grid)
+        env = bm.envelope(bm.analytic_signal(img.data, axis=0))
+        iz, ix = np.unravel_index(env.argmax(), env.shape)
+        assert abs(iz - np.abs(grid.z_positions - scat[1]).argmin()) <= 1
+        assert abs(ix - np.abs(grid.x_positions - scat[0]).argmin()) <= 1
+
+
+def test_seeded_benchmark_outputs_identical():
+    ph = bm.Phantom(((0.2e-3, 6e-3, 1.0),), center_frequency=5e6, n_cycles=2)
+    ctx = bm.AcquisitionContext(1540.0, 40e6, 24, 2e-4, bm.StaScheme(tuple(range(24))))
+    graph = bm.build_graph(bm.bmode_chain())
+
+    def run():
+        env = bm.open_simulator(ph, ctx, 512, seed=11, noise_std=0.1)
+        return bm.benchmark(graph, env, n_frames=2, warmup=1, keep_outputs=True)
+
+    r1, r2 = run(), run()
+    for o1, o2 in zip(r1.outputs, r2.outputs):
+        assert (o1["dynamic_adjustment"].numpy().tobytes()
+                == o2["dynamic_adjustment"].numpy().tobytes())
+    assert r1.timing.total_ms > 0

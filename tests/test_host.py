@@ -1,0 +1,117 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol declared
+in include/bmode200.h (no compute without a GPU), the host-side contract
+(types, errors, graph building) behaves like the reference's, and the
+product path refuses to run without CUDA instead of falling back."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1811_01566_b200 as bm
+from paper_1811_01566_b200 import _native as N
+from paper_1811_01566_b200 import build as B
+from paper_1811_01566_b200.errors import (CycleDetected, DimensionMismatch, InvalidMetadata,
+                                          NativeError, PortMismatch, UnknownOperator)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "bmode200.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(bm_\w+)\(", src, re.M)))
+
+
+def test_library_built_for_sm100a_and_exports_header_symbols():
+    lib_path = B.build()
+    lib = ctypes.CDLL(lib_path)
+    syms = header_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(N.SIGNATURES), "ctypes signatures out of sync with the header"
+    lib.bm_abi_version.restype = ctypes.c_int
+    assert lib.bm_abi_version() == 1
+    lib.bm_error_string.restype = ctypes.c_char_p
+    assert lib.bm_error_string(4) == b"analytic signal needs axis length >= 2"
+
+
+def test_library_contains_sm100a_code():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_geometry_struct_layout():
+    # 12 int32 + 2 double + 10 pointers, no padding surprises
+    assert ctypes.sizeof(N.DasGeometry) == 12 * 4 + 2 * 8 + 10 * 8
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    lib = N.load()
+    g = N.DasGeometry()
+    assert lib.bm_das_beamform(ctypes.byref(g), None, 0, None, 0, 1, None) == 1
+    assert lib.bm_analytic_signal(0, None, None, 1, 8, 1, None) == 1
+    assert lib.bm_display(0, None, None, None, None, 1, 4, 30.0, None) == 1
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    ctx = bm.AcquisitionContext(1540.0, 40e6, 4, 2e-4, bm.StaScheme((0, 1, 2, 3)))
+    grid = bm.ImageGrid(np.linspace(-1e-3, 1e-3, 4), np.linspace(1e-3, 2e-3, 4))
+    frame = bm.RfFrame(np.zeros((4, 4, 64), np.float32))
+    with pytest.raises(NativeError):
+        bm.das_beamform(frame, ctx, grid)
+    with pytest.raises(NativeError):
+        bm.analytic_signal(np.ones(8))
+
+
+def test_types_mirror_reference_validation():
+    with pytest.raises(InvalidMetadata):
+        bm.RfFrame(np.array([[[np.nan]]]))
+    with pytest.raises(DimensionMismatch):
+        bm.RfFrame(np.zeros((2, 2)))
+    with pytest.raises(InvalidMetadata):
+        bm.PwScheme((2.0,))
+    ctx = bm.AcquisitionContext(1540.0, 40e6, 8, 2e-4, bm.StaScheme(tuple(range(8))))
+    with pytest.raises(InvalidMetadata):
+        ctx.channel_elements(4)
+    with pytest.raises(DimensionMismatch):
+        bm.validate_pair(bm.RfFrame(np.zeros((3, 8, 16))), ctx)
+    g = bm.default_grid(ctx, 256, "sta")
+    assert g.shape == (256, 8)
+    m = bm.centered_rx_map(128, 64, range(128))
+    assert m.shape == (128, 64) and m.min() == 0 and m.max() == 127
+
+
+def test_graph_building_like_reference():
+    graph = bm.build_graph(bm.bmode_chain())
+    assert graph.order == ["beamform", "analytic_signal", "envelope", "dynamic_adjustment"]
+    spec = bm.bmode_chain()
+    spec["nodes"][0]["kind"] = "warp"
+    with pytest.raises(UnknownOperator):
+        bm.build_graph(spec)
+    spec = {"nodes": [{"name": "a", "kind": "identity"}, {"name": "b", "kind": "identity"},
+                      {"name": "c", "kind": "identity"}],
+            "edges": [{"from": "b", "to": "c"}, {"from": "c", "to": "b"}],
+            "inputs": ["a"], "outputs": ["a"]}
+    with pytest.raises(CycleDetected):
+        bm.build_graph(spec)
+    spec = bm.bmode_chain()
+    spec["edges"].append({"from": "beamform", "to": "envelope"})
+    with pytest.raises(PortMismatch):
+        bm.build_graph(spec)
+
+
+def test_register_into_foreign_registry():
+    reg = {}
+    kinds = bm.register_gpu_operators(registry=reg)
+    assert sorted(reg) == ["analytic_signal", "beamform", "dynamic_adjustment", "envelope"]
+    assert {k.name: (k.input_kinds, k.output_kind) for k in kinds}["beamform"] == (
+        ("observation",), "rf_image")
