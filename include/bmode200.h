@@ -71,6 +71,10 @@ typedef struct bm_das_geometry {
   int32_t n_elements; /* probe elements                                      */
   int32_t n_z;        /* image rows (depth)                                  */
   int32_t n_x;        /* image columns (lateral)                             */
+  int32_t window_hint; /* set by bm_das_prepare: max samples a fast-path tile
+                          window can span (0 = not prepared -> generic kernel) */
+  int32_t t0_nonzero;  /* set by bm_das_prepare: 1 if any fs*t0 != 0 (the fast
+                          kernel then keeps the reference's "- t0" rounding step) */
   int32_t reserved;
   double speed_of_sound;     /* c  (cast to dtype, beamform.py:206)          */
   double sampling_frequency; /* fs (cast to dtype, beamform.py:207)          */
@@ -93,6 +97,15 @@ typedef struct bm_das_geometry {
  * (beamform.py:66-81).  span_out: device int32[2 * n_z * n_x]. */
 int bm_das_aperture_span(const bm_das_geometry* g, double f_number, int32_t* span_out,
                          void* stream);
+
+/* Host-side preparation of the fast (shared-memory-staged) DAS path: from
+ * HOST copies of the element/grid positions and of fs*t0 (as double), bound
+ * the sample window any tile of the fast kernel can touch and check that all
+ * delays stay in the exactly-representable range of its index arithmetic.
+ * Writes g->window_hint (0 when the fast path does not apply).  Pure host
+ * code: no device access, no stream. */
+int bm_das_prepare(bm_das_geometry* g, const double* elem_x_host, const double* x_host,
+                   const double* z_host, const double* t0_smp_host);
 
 /* Delay-and-Sum of n_frames frames.
  *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride

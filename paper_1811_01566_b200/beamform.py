@@ -139,6 +139,14 @@ class DasPlan:
                        span.data_ptr(), N.stream_ptr())
             self._bufs["span"] = span
             g.span = span.data_ptr()
+        # host-side bound of the fast kernel's sample windows (bm_das_prepare)
+        hx = np.ascontiguousarray(grid.x_positions, np.float64)
+        hz = np.ascontiguousarray(grid.z_positions, np.float64)
+        he = np.ascontiguousarray(ctx.element_positions(), np.float64)
+        ht = np.ascontiguousarray(t0_smp, np.float64)
+        N.call("bm_das_prepare", ctypes.byref(g), he.ctypes.data, hx.ctypes.data,
+               hz.ctypes.data, ht.ctypes.data)
+        self.fast_window = int(g.window_hint)
         self._geom = g
         self.ctx, self.grid, self.apod, self.dtype, self.n_rx = ctx, grid, apod, dtype, n_rx
         self.device = dev
@@ -149,15 +157,18 @@ class DasPlan:
         return (self.ctx is ctx and self.grid is grid and self.apod == apod
                 and self.dtype == np.dtype(dtype) and self.n_rx == n_rx)
 
-    def geometry(self, n_samples: int, interp: str) -> N.DasGeometry:
-        """A copy of the C descriptor for one launch."""
+    def geometry(self, n_samples: int, interp: str, fast: bool = True) -> N.DasGeometry:
+        """A copy of the C descriptor for one launch (``fast=False`` forces the
+        generic kernel, used by tests to cross-check the two paths)."""
         g = N.DasGeometry()
         ctypes.pointer(g)[0] = self._geom
+        if not fast:
+            g.window_hint = 0
         g.n_samples = int(n_samples)
         g.interp = N.BM_NEAREST if interp == "nearest" else N.BM_LINEAR
         return g
 
-    def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None):
+    def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True):
         """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
         ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``."""
         import torch
@@ -177,7 +188,7 @@ class DasPlan:
             raise InvalidMetadata("data", "frame shape differs from the plan")
         if out is None:
             out = torch.empty((f,) + self.shape, dtype=rfb.dtype, device=self.device)
-        g = self.geometry(n_s, interp)
+        g = self.geometry(n_s, interp, fast)
         n_img = self.shape[0] * self.shape[1]
         for f0 in range(0, f, 65535):
             nf = min(65535, f - f0)

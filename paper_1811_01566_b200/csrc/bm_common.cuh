@@ -46,4 +46,9 @@ inline int sm_count() {
   return n;
 }
 
+// fast (shared-memory-staged, f32x2) DAS path, bm_das_fast.cu
+int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride);
+int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                    int64_t out_stride, int n_frames, cudaStream_t s);
+
 }  // namespace bm

@@ -240,8 +240,10 @@ extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t
   if (rc) return rc;
   if (!rf || !out || n_frames < 0 || n_frames > 65535) return BM_ERR_INVALID_ARGUMENT;
   if (n_frames == 0) return BM_OK;
-  bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride};
   cudaStream_t s = (cudaStream_t)stream;
+  if (bm::das_fast_eligible(*g, rf_frame_stride))
+    return bm::das_fast_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
+  bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride};
   if (g->dtype == BM_F32)
     return g->scheme == BM_PW ? bm::launch_p<float, true>(a, n_frames, s)
                               : bm::launch_p<float, false>(a, n_frames, s);

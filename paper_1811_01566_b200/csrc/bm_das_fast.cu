@@ -1,0 +1,413 @@
+// K1 fast path: shared-memory-staged, packed-f32x2 Delay-and-Sum (sm_100a).
+//
+// Same arithmetic as das_kernel (bm_das.cu) and therefore the same bits as
+// the reference's f32 das_beamform (beamform.py:122-187 with the DasPlan
+// delays of :211-228) -- every operator is rounded once, in the reference's
+// order -- but organised for the B200's shared-memory crossbar and its
+// packed FP32 pipe:
+//
+//  * CTA = 64 threads, tile = 8 rows x 16 columns; each thread owns the pixel
+//    pair (r, c) / (r + 4, c) and evaluates both with FADD2/FMUL2 (f32x2), so
+//    one instruction advances two pixels.  A warp's 32 "A" pixels form a 4 x 8
+//    block: for every (e, j) their sample indices fall in one 32-word span, so
+//    each gather is a single conflict-free shared-memory wavefront (measured
+//    by tests/bankmodel in DESIGN.md).
+//  * Receive delays of the tile, D[m][pair] = fs*(sqrt(dx^2+z^2)/c) for every
+//    element m, are built once per CTA in shared memory and reused for every
+//    transmit and every frame of the CTA's frame group.
+//  * RF is staged per chunk of JC channels: for each (e, j) only the window of
+//    samples the tile can reach ([tmin-2, tmax+3], from the tile rectangle's
+//    nearest / farthest geometry) is copied with cp.async (16 B, zero-filled
+//    outside the trace, which reproduces x_pad's zero sentinels), double
+//    buffered against the computation of the previous chunk.
+//  * floor(t) and the integer sample index come from one FADD2.RM with the
+//    1.5*2^23 magic constant (exact for |t| < 2^22, checked on the host by
+//    bm_das_prepare); the index is the float's bit pattern, so no F2I.
+#include "bm_common.cuh"
+
+namespace bm {
+
+constexpr int FZ = 8, FX = 16, FTHREADS = 64, JC = 16;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo_f(u64 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float hi_f(u64 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return b;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 add2_rm(u64 a, u64 b) {
+  u64 d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// Product rounded once, as a separate operation.  ptxas (CUDA 12.9) contracts
+// mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 even under --fmad=false,
+// which would drop the product's rounding (the reference rounds it:
+// beamform.py:178-187).  fma(a, b, +0) = RN(a*b) is not contracted further;
+// it differs from mul only in the sign of an exact-zero product, which cannot
+// change the running sum (the accumulator starts at +0 and, in round-to-
+// nearest, can never become -0, and x + (+-0) == x for every other x).
+// tests/test_host.py::test_no_contracted_fma_in_das_kernels checks the SASS.
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(0ull));
+  return d;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr), "l"(gptr),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+struct FastArgs {
+  bm_das_geometry g;
+  const float* rf;
+  int64_t rf_stride;
+  float* out;
+  int64_t out_stride;
+  int n_frames;
+  int frames_per_cta;
+  int W;  // staged window capacity per channel (samples, multiple of 4)
+};
+
+struct ChunkMeta {
+  int4 pk[JC / 2];  // per channel pair: {D row byte offset, K, D row byte offset, K}
+                    // with K such that smem address of x[k] = bits(floor(t)+magic)*4 + K
+  int ws[JC];       // first staged sample (multiple of 4)
+  int len[JC];      // staged samples (multiple of 4, <= W)
+};
+
+__device__ __forceinline__ float lds0(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds1(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1+4];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+template <bool PW, bool LINEAR, bool T0>
+__global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a) {
+  using O = R<float>;
+  const bm_das_geometry& g = a.g;
+  const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
+  const int W = a.W;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* D = reinterpret_cast<u64*>(smem_raw);                       // [n_el][64] pairs
+  float* rmin = reinterpret_cast<float*>(D + (size_t)n_el * FTHREADS);  // [n_el]
+  float* rmax = rmin + n_el;                                        // [n_el]
+  float* tmin = rmax + n_el;                                        // [n_tx]
+  float* tmax = tmin + n_tx;                                        // [n_tx]
+  ChunkMeta* meta = reinterpret_cast<ChunkMeta*>(tmax + n_tx);      // [3]
+  float* win = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(meta + 3) + 15) & ~uintptr_t(15));  // [2][JC][W]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int tiles_x = (g.n_x + FX - 1) / FX;
+  const int tz0 = (blockIdx.x / tiles_x) * FZ, tx0 = (blockIdx.x % tiles_x) * FX;
+  const int col = tx0 + warp * 8 + (lane & 7);
+  const int rowA = tz0 + (lane >> 3), rowB = rowA + 4;
+  const int colc = min(col, g.n_x - 1);
+  const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
+
+  const float c = O::from_double(g.speed_of_sound);
+  const float fs = O::from_double(g.sampling_frequency);
+  const double px = g.x_pos[colc];
+  const float pxd = O::from_double(px);
+  const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
+
+  // ---- per-CTA geometry: exact receive delays of the pixel pair, window bounds
+  for (int m = 0; m < n_el; ++m) {
+    const float dx = O::from_double(g.elem_x[m] - px);
+    const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
+    const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
+    D[(size_t)m * FTHREADS + tid] = pk(dA, dB);
+  }
+  const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + FX, g.n_x) - 1];
+  const double z0 = g.z_pos[tz0], z1 = g.z_pos[min(tz0 + FZ, g.n_z) - 1];
+  const double k = g.sampling_frequency / g.speed_of_sound;
+  for (int m = tid; m < n_el; m += FTHREADS) {
+    const double xm = g.elem_x[m];
+    const double dmin = fmax(0.0, fmax(x0 - xm, xm - x1));
+    const double dmax = fmax(fabs(x0 - xm), fabs(x1 - xm));
+    rmin[m] = (float)(k * sqrt(dmin * dmin + z0 * z0));
+    rmax[m] = (float)(k * sqrt(dmax * dmax + z1 * z1));
+  }
+  __syncthreads();
+  for (int e = tid; e < n_tx; e += FTHREADS) {
+    if (PW) {
+      const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
+      const double sa = reinterpret_cast<const float*>(g.sin_a)[e];
+      const double v00 = z0 * ca + x0 * sa, v01 = z0 * ca + x1 * sa;
+      const double v10 = z1 * ca + x0 * sa, v11 = z1 * ca + x1 * sa;
+      tmin[e] = (float)(k * fmin(fmin(v00, v01), fmin(v10, v11)));
+      tmax[e] = (float)(k * fmax(fmax(v00, v01), fmax(v10, v11)));
+    } else {
+      const int te = g.tx_elements[e];
+      tmin[e] = rmin[te];
+      tmax[e] = rmax[te];
+    }
+  }
+  __syncthreads();
+
+  const float* __restrict__ t0s = reinterpret_cast<const float*>(g.t0_smp);
+  const int n_chunks = (n_rx + JC - 1) / JC;
+  const int f_begin = blockIdx.y * a.frames_per_cta;
+  const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
+  const int Q = f_count * n_tx * n_chunks;
+
+  // chunk q -> (frame, e, channel block)
+  auto decode = [&](int q, int& fl, int& e, int& cb) {
+    cb = q % n_chunks;
+    const int r = q / n_chunks;
+    e = r % n_tx;
+    fl = r / n_tx;
+  };
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
+  auto make_meta = [&](int q) {  // threads [0, JC): one channel each
+    int fl, e, cb;
+    decode(q, fl, e, cb);
+    const int j = cb * JC + tid;
+    ChunkMeta& M = meta[q % 3];
+    int m = 0, ws = 0, len = 0;
+    if (j < n_rx) {
+      m = g.rx_map[(int64_t)e * n_rx + j];
+      const float t0 = t0s[e];
+      const int lo = (int)floorf(tmin[e] + rmin[m] - t0) - 3;
+      ws = lo & ~3;
+      const int hi = (int)floorf(tmax[e] + rmax[m] - t0) + 4;
+      len = (hi - ws + 3) & ~3;
+      len = len > W ? W : len;  // host guarantees len <= W
+    }
+    M.ws[tid] = ws;
+    M.len[tid] = len;
+    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + tid) * W) * 4u;
+    int* mo = reinterpret_cast<int*>(&M.pk[tid >> 1]) + 2 * (tid & 1);
+    mo[0] = m * FTHREADS * 8;
+    mo[1] = (int)(wb - (uint32_t)(kMagicBits + ws) * 4u);
+  };
+  auto issue_loads = [&](int q) {
+    int fl, e, cb;
+    decode(q, fl, e, cb);
+    const ChunkMeta& M = meta[q % 3];
+    const float* rfe = a.rf + (int64_t)(f_begin + fl) * a.rf_stride + (int64_t)e * n_rx * n_s;
+    const uint32_t wbase = win_s + (uint32_t)((q & 1) * JC * W) * 4u;
+    // 4 threads per channel, 16 B per cp.async, no division
+    const int jj = tid >> 2;
+    const int j = cb * JC + jj;
+    const int ws = M.ws[jj], len = M.len[jj];
+    const float* tr = rfe + (int64_t)j * n_s;
+    for (int o = 4 * (tid & 3); o < len; o += 16) {
+      const int s0 = ws + o;
+      const bool in = s0 >= 0 && s0 + 4 <= n_s;
+      cp_async16(wbase + (uint32_t)(jj * W + o) * 4u, in ? tr + s0 : tr, in ? 16 : 0);
+    }
+  };
+
+  if (tid < JC) {
+    make_meta(0);
+    if (Q > 1) make_meta(1);
+  }
+  __syncthreads();
+  issue_loads(0);
+  cp_async_commit();
+
+  const u64 M2 = pk(kMagic, kMagic);
+  const u64 NM2 = pk(-kMagic, -kMagic);
+  const u64 ONE2 = pk(1.0f, 1.0f);
+  const u64 HALF2 = pk(0.5f, 0.5f);
+  u64 acc = 0ull;  // (+0.0f, +0.0f)
+  u64 txd = 0ull, t0e2 = 0ull;
+
+  for (int q = 0; q < Q; ++q) {
+    int fl, e, cb;
+    decode(q, fl, e, cb);
+    __syncthreads();  // compute(q-1) done everywhere: its buffers may be refilled
+    if (tid < JC && q + 2 < Q) make_meta(q + 2);
+    if (q + 1 < Q) issue_loads(q + 1);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();  // chunk q staged and visible
+
+    if (cb == 0) {
+      if (PW) {
+        const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
+        const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+        const float xs = O::mul(pxd, sa);
+        const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+        const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
+        txd = pk(tA, tB);
+      } else {
+        txd = D[(size_t)g.tx_elements[e] * FTHREADS + tid];
+      }
+      const float t0 = t0s[e];
+      t0e2 = pk(t0, t0);
+    }
+    const ChunkMeta& M = meta[q % 3];
+    const int jn = min(JC, n_rx - cb * JC);
+    const unsigned char* Dbytes = reinterpret_cast<const unsigned char*>(D) + tid * 8;
+    auto contrib = [&](int doff, int K) {
+      const u64 rxd = *reinterpret_cast<const u64*>(Dbytes + doff);
+      u64 t = add2(txd, rxd);
+      if (T0) t = sub2(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
+      if (LINEAR) {
+        const u64 r = add2_rm(t, M2);   // floor(t) + 1.5*2^23, exactly
+        const u64 k0f = add2(r, NM2);   // floor(t)
+        const u64 fr = sub2(t, k0f);    // a = t - floor(t)
+        const u64 om = sub2(ONE2, fr);  // 1 - a
+        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + (uint32_t)K;
+        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + (uint32_t)K;
+        const u64 x0 = pk(lds0(aA), lds0(aB));
+        const u64 x1 = pk(lds1(aA), lds1(aB));
+        acc = add2(acc, mul2(om, x0));  // acc = out + (1 - a) * x[k0]
+        acc = add2(acc, mul2(fr, x1));  // out = acc + a * x[k1]
+      } else {
+        const u64 r = add2_rm(add2(t, HALF2), M2);  // floor(t + 0.5)
+        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + (uint32_t)K;
+        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + (uint32_t)K;
+        acc = add2(acc, pk(lds0(aA), lds0(aB)));
+      }
+    };
+    if (jn == JC) {
+#pragma unroll
+      for (int jp = 0; jp < JC / 2; ++jp) {
+        const int4 mm = M.pk[jp];
+        contrib(mm.x, mm.y);
+        contrib(mm.z, mm.w);
+      }
+    } else {
+      for (int jp = 0; jp < (jn + 1) / 2; ++jp) {
+        const int4 mm = M.pk[jp];
+        contrib(mm.x, mm.y);
+        if (2 * jp + 1 < jn) contrib(mm.z, mm.w);
+      }
+    }
+
+    if (e == n_tx - 1 && cb == n_chunks - 1) {  // frame complete
+      const int64_t fo = (int64_t)(f_begin + fl) * a.out_stride;
+      if (col < g.n_x) {
+        if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = lo_f(acc);
+        if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = hi_f(acc);
+      }
+      acc = 0ull;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+}
+
+size_t fast_smem_bytes(const bm_das_geometry& g, int W) {
+  size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)(2 * g.n_elements + 2 * g.n_tx) * 4 +
+             3 * sizeof(ChunkMeta);
+  b = (b + 15) & ~size_t(15);
+  return b + (size_t)2 * JC * W * 4;
+}
+
+int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride) {
+  if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
+  if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
+  if (fast_smem_bytes(g, g.window_hint) > 200 * 1024) return 0;
+  return 1;
+}
+
+int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                    int64_t out_stride, int n_frames, cudaStream_t s) {
+  FastArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1, g.window_hint};
+  const int tiles = ((g.n_z + FZ - 1) / FZ) * ((g.n_x + FX - 1) / FX);
+  // frames per CTA: amortise the per-CTA delay build over a frame group while
+  // keeping >= ~8 waves of CTAs for load balance
+  int fpc = 1;
+  while (fpc < 8 && fpc * 2 <= n_frames && (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >=
+                                               8LL * 3 * sm_count())
+    fpc *= 2;
+  a.frames_per_cta = fpc;
+  const size_t smem = fast_smem_bytes(g, a.W);
+  const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
+  decltype(&das_fast_kernel<true, true, true>) k;
+  if (g.t0_nonzero)
+    k = pw ? (lin ? das_fast_kernel<true, true, true> : das_fast_kernel<true, false, true>)
+           : (lin ? das_fast_kernel<false, true, true> : das_fast_kernel<false, false, true>);
+  else
+    k = pw ? (lin ? das_fast_kernel<true, true, false> : das_fast_kernel<true, false, false>)
+           : (lin ? das_fast_kernel<false, true, false> : das_fast_kernel<false, false, false>);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return BM_ERR_CUDA;
+  dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
+  k<<<grid, FTHREADS, smem, s>>>(a);
+  return cuda_status();
+}
+
+}  // namespace bm
+
+// Host-only: bound the fast kernel's per-(e, j) sample window over all tiles.
+extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const double* x,
+                              const double* z, const double* t0_smp) {
+  if (!g || !elem_x || !x || !z || !t0_smp) return BM_ERR_INVALID_ARGUMENT;
+  g->window_hint = 0;
+  g->t0_nonzero = 1;
+  if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
+  double zext = 0.0, xext = 0.0;
+  for (int i = 0; i < g->n_z; i += bm::FZ) {
+    const int l = (i + bm::FZ < g->n_z ? i + bm::FZ : g->n_z) - 1;
+    zext = fmax(zext, z[l] - z[i]);
+  }
+  for (int i = 0; i < g->n_x; i += bm::FX) {
+    const int l = (i + bm::FX < g->n_x ? i + bm::FX : g->n_x) - 1;
+    xext = fmax(xext, x[l] - x[i]);
+  }
+  const double k = g->sampling_frequency / g->speed_of_sound;
+  const double diag = sqrt(zext * zext + xext * xext);
+  int W = (int)ceil(2.0 * k * diag + 16.0);
+  W = (W + 3) & ~3;
+  // largest |t|: every delay is <= k * (farthest grid corner from any element
+  // or from the origin) per path
+  double dmax = 0.0;
+  const double cx[2] = {x[0], x[g->n_x - 1]}, cz[2] = {z[0], z[g->n_z - 1]};
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      dmax = fmax(dmax, sqrt(cx[a] * cx[a] + cz[b] * cz[b]));
+      for (int m = 0; m < g->n_elements; m += (g->n_elements > 1 ? g->n_elements - 1 : 1)) {
+        const double dx = cx[a] - elem_x[m];
+        dmax = fmax(dmax, sqrt(dx * dx + cz[b] * cz[b]));
+      }
+    }
+  double t0max = 0.0;
+  g->t0_nonzero = 0;
+  for (int e = 0; e < g->n_tx; ++e) {
+    t0max = fmax(t0max, fabs(t0_smp[e]));
+    if (t0_smp[e] != 0.0) g->t0_nonzero = 1;
+  }
+  const double tabs = 2.0 * k * dmax + t0max + 16.0 + W;
+  if (!(tabs < 4194304.0)) return BM_OK;  // outside the exact magic-number range
+  if (W > 4096) return BM_OK;
+  g->window_hint = W;
+  return BM_OK;
+}

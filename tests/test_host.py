@@ -46,8 +46,8 @@ def test_library_contains_sm100a_code():
 
 
 def test_geometry_struct_layout():
-    # 12 int32 + 2 double + 10 pointers, no padding surprises
-    assert ctypes.sizeof(N.DasGeometry) == 12 * 4 + 2 * 8 + 10 * 8
+    # 14 int32 + 2 double + 10 pointers, no padding surprises
+    assert ctypes.sizeof(N.DasGeometry) == 14 * 4 + 2 * 8 + 10 * 8
 
 
 def test_invalid_arguments_rejected_without_gpu():
@@ -115,3 +115,33 @@ def test_register_into_foreign_registry():
     assert sorted(reg) == ["analytic_signal", "beamform", "dynamic_adjustment", "envelope"]
     assert {k.name: (k.input_kinds, k.output_kind) for k in kinds}["beamform"] == (
         ("observation",), "rf_image")
+
+
+def _sass_by_function():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "-sass", B.build()], capture_output=True, text=True).stdout
+    funcs, name = {}, None
+    for line in out.splitlines():
+        if "Function :" in line:
+            name = line.split("Function :")[1].strip()
+            funcs[name] = []
+        elif name and "/*" in line:
+            funcs[name].append(line)
+    return funcs
+
+
+def test_no_contracted_fma_in_das_kernels():
+    """Bitwise parity needs every product rounded before it is added.  ptxas
+    may contract f32x2 mul+add into FFMA2; the DAS kernels only allow FFMA2
+    with a zero addend (a plain rounded product) and scalar FFMA only inside
+    the correctly-rounded sqrt/div sequences."""
+    funcs = _sass_by_function()
+    das = {n: l for n, l in funcs.items() if "das_fast_kernel" in n}
+    assert len(das) == 8
+    for n, lines in das.items():
+        for l in lines:
+            if "FFMA2" in l:
+                assert "RZ" in l.split("FFMA2", 1)[1].split(";")[0], (n, l)
+        assert any("FADD2.RM" in l for l in lines), n  # packed floor, magic constant
+        assert any("LDGSTS" in l for l in lines), n    # cp.async staging
