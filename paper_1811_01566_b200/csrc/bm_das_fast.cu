@@ -16,10 +16,12 @@
 //    element m, are built once per CTA in shared memory and reused for every
 //    transmit and every frame of the CTA's frame group.
 //  * RF is staged per chunk of JC channels: for each (e, j) only the window of
-//    samples the tile can reach ([tmin-2, tmax+3], from the tile rectangle's
-//    nearest / farthest geometry) is copied with cp.async (16 B, zero-filled
-//    outside the trace, which reproduces x_pad's zero sentinels), double
-//    buffered against the computation of the previous chunk.
+//    samples the tile can reach ([tmin-3, tmax+4], from the tile rectangle's
+//    nearest / farthest geometry) is copied by the TMA bulk-copy engine
+//    (cp.async.bulk, one instruction per channel, completion on an mbarrier),
+//    double buffered against the computation of the previous chunk.  Window
+//    samples outside the trace are zeroed, reproducing x_pad's zero
+//    sentinels (beamform.py:127-137, :273-274).
 //  * floor(t) and the integer sample index come from one FADD2.RM with the
 //    1.5*2^23 magic constant (exact for |t| < 2^22, checked on the host by
 //    bm_das_prepare); the index is the float's bit pattern, so no F2I.
@@ -39,14 +41,10 @@ __device__ __forceinline__ u64 pk(float a, float b) {
   return r;
 }
 __device__ __forceinline__ float lo_f(u64 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  return a;
+  return __uint_as_float((unsigned)(r & 0xffffffffu));
 }
 __device__ __forceinline__ float hi_f(u64 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  return b;
+  return __uint_as_float((unsigned)(r >> 32));
 }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   u64 d;
@@ -77,12 +75,6 @@ __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
   return d;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr), "l"(gptr),
-               "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 struct FastArgs {
   bm_das_geometry g;
@@ -98,8 +90,6 @@ struct FastArgs {
 struct ChunkMeta {
   int4 pk[JC / 2];  // per channel pair: {D row byte offset, K, D row byte offset, K}
                     // with K such that smem address of x[k] = bits(floor(t)+magic)*4 + K
-  int ws[JC];       // first staged sample (multiple of 4)
-  int len[JC];      // staged samples (multiple of 4, <= W)
 };
 
 __device__ __forceinline__ float lds0(uint32_t a) {
@@ -113,6 +103,47 @@ __device__ __forceinline__ float lds1(uint32_t a) {
   return v;
 }
 
+// ---- TMA (bulk copy engine) + mbarrier helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// Chunk cursor: q -> (frame in group, transmit e, channel block cb), advanced
+// incrementally (no integer division in the loop).
+struct Cursor {
+  int fl, e, cb;
+  __device__ __forceinline__ void next(int n_chunks, int n_tx) {
+    if (++cb == n_chunks) {
+      cb = 0;
+      if (++e == n_tx) {
+        e = 0;
+        ++fl;
+      }
+    }
+  }
+};
+
 template <bool PW, bool LINEAR, bool T0>
 __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a) {
   using O = R<float>;
@@ -121,14 +152,16 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const int W = a.W;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* D = reinterpret_cast<u64*>(smem_raw);                       // [n_el][64] pairs
+  u64* D = reinterpret_cast<u64*>(smem_raw);                            // [n_el][64] pairs
   float* rmin = reinterpret_cast<float*>(D + (size_t)n_el * FTHREADS);  // [n_el]
-  float* rmax = rmin + n_el;                                        // [n_el]
-  float* tmin = rmax + n_el;                                        // [n_tx]
-  float* tmax = tmin + n_tx;                                        // [n_tx]
-  ChunkMeta* meta = reinterpret_cast<ChunkMeta*>(tmax + n_tx);      // [3]
+  float* rmax = rmin + n_el;                                             // [n_el]
+  float* tmin = rmax + n_el;                                             // [n_tx]
+  float* tmax = tmin + n_tx;                                             // [n_tx]
+  ChunkMeta* meta = reinterpret_cast<ChunkMeta*>(
+      (reinterpret_cast<uintptr_t>(tmax + n_tx) + 15) & ~uintptr_t(15));  // [2]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + 2);                // [2]
   float* win = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(meta + 3) + 15) & ~uintptr_t(15));  // [2][JC][W]
+      (reinterpret_cast<uintptr_t>(mbar + 2) + 15) & ~uintptr_t(15));    // [2][JC][W]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -144,6 +177,14 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const double px = g.x_pos[colc];
   const float pxd = O::from_double(px);
   const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(mbar);
+
+  if (tid == 0) {
+    mbar_init(bar_s, 1);
+    mbar_init(bar_s + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
 
   // ---- per-CTA geometry: exact receive delays of the pixel pair, window bounds
   for (int m = 0; m < n_el; ++m) {
@@ -185,61 +226,47 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
   const int Q = f_count * n_tx * n_chunks;
 
-  // chunk q -> (frame, e, channel block)
-  auto decode = [&](int q, int& fl, int& e, int& cb) {
-    cb = q % n_chunks;
-    const int r = q / n_chunks;
-    e = r % n_tx;
-    fl = r / n_tx;
-  };
-  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
-  auto make_meta = [&](int q) {  // threads [0, JC): one channel each
-    int fl, e, cb;
-    decode(q, fl, e, cb);
-    const int j = cb * JC + tid;
-    ChunkMeta& M = meta[q % 3];
+  // Producer (warp 0, lane jj = one channel of the chunk): window bounds,
+  // meta for the consumers, zero fill of the out-of-trace part, one bulk copy.
+  auto produce = [&](int q, const Cursor& cu) {
+    const int buf = q & 1;
+    const int j = cu.cb * JC + lane;
     int m = 0, ws = 0, len = 0;
-    if (j < n_rx) {
-      m = g.rx_map[(int64_t)e * n_rx + j];
-      const float t0 = t0s[e];
-      const int lo = (int)floorf(tmin[e] + rmin[m] - t0) - 3;
-      ws = lo & ~3;
-      const int hi = (int)floorf(tmax[e] + rmax[m] - t0) + 4;
-      len = (hi - ws + 3) & ~3;
-      len = len > W ? W : len;  // host guarantees len <= W
+    if (lane < JC && j < n_rx) {
+      m = g.rx_map[(int64_t)cu.e * n_rx + j];
+      const float t0 = t0s[cu.e];
+      ws = ((int)floorf(tmin[cu.e] + rmin[m] - t0) - 3) & ~3;
+      const int hi = (int)floorf(tmax[cu.e] + rmax[m] - t0) + 4;
+      len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
     }
-    M.ws[tid] = ws;
-    M.len[tid] = len;
-    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + tid) * W) * 4u;
-    int* mo = reinterpret_cast<int*>(&M.pk[tid >> 1]) + 2 * (tid & 1);
-    mo[0] = m * FTHREADS * 8;
-    mo[1] = (int)(wb - (uint32_t)(kMagicBits + ws) * 4u);
-  };
-  auto issue_loads = [&](int q) {
-    int fl, e, cb;
-    decode(q, fl, e, cb);
-    const ChunkMeta& M = meta[q % 3];
-    const float* rfe = a.rf + (int64_t)(f_begin + fl) * a.rf_stride + (int64_t)e * n_rx * n_s;
-    const uint32_t wbase = win_s + (uint32_t)((q & 1) * JC * W) * 4u;
-    // 4 threads per channel, 16 B per cp.async, no division
-    const int jj = tid >> 2;
-    const int j = cb * JC + jj;
-    const int ws = M.ws[jj], len = M.len[jj];
-    const float* tr = rfe + (int64_t)j * n_s;
-    for (int o = 4 * (tid & 3); o < len; o += 16) {
-      const int s0 = ws + o;
-      const bool in = s0 >= 0 && s0 + 4 <= n_s;
-      cp_async16(wbase + (uint32_t)(jj * W + o) * 4u, in ? tr + s0 : tr, in ? 16 : 0);
+    const int v0 = max(ws, 0), v1 = min(ws + len, n_s);  // in-trace part
+    const uint32_t bytes = v1 > v0 ? (uint32_t)(v1 - v0) * 4u : 0u;
+    const uint32_t wb = win_s + (uint32_t)((buf * JC + lane) * W) * 4u;
+    if (lane < JC) {
+      float* wz = win + (buf * JC + lane) * W;
+      // zero sentinels for the part of the window outside the trace
+      for (int s0 = ws, e0 = min(v0, ws + len); s0 < e0; ++s0) wz[s0 - ws] = 0.0f;
+      for (int s0 = max(v1, ws); s0 < ws + len; ++s0) wz[s0 - ws] = 0.0f;
+      int* mo = reinterpret_cast<int*>(&meta[buf].pk[lane >> 1]) + 2 * (lane & 1);
+      mo[0] = m * FTHREADS * 8;
+      mo[1] = (int)(wb - (uint32_t)(kMagicBits + ws) * 4u);
+    }
+    uint32_t total = bytes;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(bar_s + 8 * buf, total);
+    if (bytes) {
+      const float* src = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
+                         ((int64_t)cu.e * n_rx + j) * n_s + v0;
+      bulk_g2s(wb + (uint32_t)(v0 - ws) * 4u, src, bytes, bar_s + 8 * buf);
     }
   };
 
-  if (tid < JC) {
-    make_meta(0);
-    if (Q > 1) make_meta(1);
-  }
-  __syncthreads();
-  issue_loads(0);
-  cp_async_commit();
+  Cursor cur{0, 0, 0}, nxt{0, 0, 0};
+  __syncthreads();  // barrier init visible to every thread
+  if (warp == 0) produce(0, nxt);
+  nxt.next(n_chunks, n_tx);
 
   const u64 M2 = pk(kMagic, kMagic);
   const u64 NM2 = pk(-kMagic, -kMagic);
@@ -247,34 +274,31 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const u64 HALF2 = pk(0.5f, 0.5f);
   u64 acc = 0ull;  // (+0.0f, +0.0f)
   u64 txd = 0ull, t0e2 = 0ull;
+  const unsigned char* Dbytes = reinterpret_cast<const unsigned char*>(D) + tid * 8;
 
   for (int q = 0; q < Q; ++q) {
-    int fl, e, cb;
-    decode(q, fl, e, cb);
-    __syncthreads();  // compute(q-1) done everywhere: its buffers may be refilled
-    if (tid < JC && q + 2 < Q) make_meta(q + 2);
-    if (q + 1 < Q) issue_loads(q + 1);
-    cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();  // chunk q staged and visible
+    __syncthreads();  // compute(q-1) done everywhere: buffer (q+1)&1 may be refilled
+    if (warp == 0 && q + 1 < Q) produce(q + 1, nxt);
+    nxt.next(n_chunks, n_tx);
 
-    if (cb == 0) {
+    if (cur.cb == 0) {
       if (PW) {
-        const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
-        const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+        const float ca = reinterpret_cast<const float*>(g.cos_a)[cur.e];
+        const float sa = reinterpret_cast<const float*>(g.sin_a)[cur.e];
         const float xs = O::mul(pxd, sa);
         const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
         const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
         txd = pk(tA, tB);
       } else {
-        txd = D[(size_t)g.tx_elements[e] * FTHREADS + tid];
+        txd = D[(size_t)g.tx_elements[cur.e] * FTHREADS + tid];
       }
-      const float t0 = t0s[e];
+      const float t0 = t0s[cur.e];
       t0e2 = pk(t0, t0);
     }
-    const ChunkMeta& M = meta[q % 3];
-    const int jn = min(JC, n_rx - cb * JC);
-    const unsigned char* Dbytes = reinterpret_cast<const unsigned char*>(D) + tid * 8;
+    mbar_wait(bar_s + 8 * (q & 1), (uint32_t)((q >> 1) & 1));  // chunk q landed
+
+    const ChunkMeta& M = meta[q & 1];
+    const int jn = min(JC, n_rx - cur.cb * JC);
     auto contrib = [&](int doff, int K) {
       const u64 rxd = *reinterpret_cast<const u64*>(Dbytes + doff);
       u64 t = add2(txd, rxd);
@@ -312,21 +336,21 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
       }
     }
 
-    if (e == n_tx - 1 && cb == n_chunks - 1) {  // frame complete
-      const int64_t fo = (int64_t)(f_begin + fl) * a.out_stride;
+    if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
+      const int64_t fo = (int64_t)(f_begin + cur.fl) * a.out_stride;
       if (col < g.n_x) {
         if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = lo_f(acc);
         if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = hi_f(acc);
       }
       acc = 0ull;
     }
+    cur.next(n_chunks, n_tx);
   }
-  asm volatile("cp.async.wait_all;\n" ::);
 }
 
 size_t fast_smem_bytes(const bm_das_geometry& g, int W) {
-  size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)(2 * g.n_elements + 2 * g.n_tx) * 4 +
-             3 * sizeof(ChunkMeta);
+  size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)(2 * g.n_elements + 2 * g.n_tx) * 4;
+  b = ((b + 15) & ~size_t(15)) + 2 * sizeof(ChunkMeta) + 2 * sizeof(uint64_t);
   b = (b + 15) & ~size_t(15);
   return b + (size_t)2 * JC * W * 4;
 }
