@@ -17,11 +17,12 @@
 //    transmit and every frame of the CTA's frame group.
 //  * RF is staged per chunk of JC channels: for each (e, j) only the window of
 //    samples the tile can reach ([tmin-3, tmax+4], from the tile rectangle's
-//    nearest / farthest geometry) is copied by the TMA bulk-copy engine
-//    (cp.async.bulk, one instruction per channel, completion on an mbarrier),
-//    double buffered against the computation of the previous chunk.  Window
-//    samples outside the trace are zeroed, reproducing x_pad's zero
-//    sentinels (beamform.py:127-137, :273-274).
+//    nearest / farthest geometry) is copied with cp.async (16 B per copy,
+//    src-size 0 zero fill for groups outside the trace, which reproduces
+//    x_pad's zero sentinels, beamform.py:127-137, :273-274), double buffered
+//    against the computation of the previous chunk.  (A TMA bulk-copy
+//    variant, one cp.async.bulk per channel on an mbarrier, measured slower:
+//    per-lane bulk copies serialise into a UBLKCP loop.)
 //  * floor(t) and the integer sample index come from one FADD2.RM with the
 //    1.5*2^23 magic constant (exact for |t| < 2^22, checked on the host by
 //    bm_das_prepare); the index is the float's bit pattern, so no F2I.
@@ -87,11 +88,6 @@ struct FastArgs {
   int W;  // staged window capacity per channel (samples, multiple of 4)
 };
 
-struct ChunkMeta {
-  int4 pk[JC / 2];  // per channel pair: {D row byte offset, K, D row byte offset, K}
-                    // with K such that smem address of x[k] = bits(floor(t)+magic)*4 + K
-};
-
 __device__ __forceinline__ float lds0(uint32_t a) {
   float v;
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -103,39 +99,26 @@ __device__ __forceinline__ float lds1(uint32_t a) {
   return v;
 }
 
-// ---- TMA (bulk copy engine) + mbarrier helpers
-__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr), "l"(gptr),
+               "r"(src_bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
 }
 
 // Chunk cursor: q -> (frame in group, transmit e, channel block cb), advanced
-// incrementally (no integer division in the loop).
+// incrementally (no integer division in the loop).  T = fl * n_tx + e.
 struct Cursor {
-  int fl, e, cb;
+  int fl, e, cb, T;
   __device__ __forceinline__ void next(int n_chunks, int n_tx) {
     if (++cb == n_chunks) {
       cb = 0;
+      ++T;
       if (++e == n_tx) {
         e = 0;
         ++fl;
@@ -144,6 +127,11 @@ struct Cursor {
   }
 };
 
+// Per-transmit staging metadata, one int2 per receive channel j:
+//   x = element m's D row byte offset (m * 64 threads * 8 B, < 2^18)
+//       | staged length (samples, multiple of 4, <= W) << 18,
+//   y = 4 * ws (first staged sample, a multiple of 4).
+// Ring of 2 transmits: meta(T + 1) is written at the first chunk of T.
 template <bool PW, bool LINEAR, bool T0>
 __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a) {
   using O = R<float>;
@@ -157,11 +145,10 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   float* rmax = rmin + n_el;                                             // [n_el]
   float* tmin = rmax + n_el;                                             // [n_tx]
   float* tmax = tmin + n_tx;                                             // [n_tx]
-  ChunkMeta* meta = reinterpret_cast<ChunkMeta*>(
-      (reinterpret_cast<uintptr_t>(tmax + n_tx) + 15) & ~uintptr_t(15));  // [2]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + 2);                // [2]
+  int2* meta = reinterpret_cast<int2*>(
+      (reinterpret_cast<uintptr_t>(tmax + n_tx) + 15) & ~uintptr_t(15));  // [2][n_rx]
   float* win = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(mbar + 2) + 15) & ~uintptr_t(15));    // [2][JC][W]
+      (reinterpret_cast<uintptr_t>(meta + 2 * n_rx) + 15) & ~uintptr_t(15));  // [2][JC][W]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -178,13 +165,6 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const float pxd = O::from_double(px);
   const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
   const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
-  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(mbar);
-
-  if (tid == 0) {
-    mbar_init(bar_s, 1);
-    mbar_init(bar_s + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
 
   // ---- per-CTA geometry: exact receive delays of the pixel pair, window bounds
   for (int m = 0; m < n_el; ++m) {
@@ -225,47 +205,46 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
   const int Q = f_count * n_tx * n_chunks;
+  const int n_T = f_count * n_tx;
 
-  // Producer (warp 0, lane jj = one channel of the chunk): window bounds,
-  // meta for the consumers, zero fill of the out-of-trace part, one bulk copy.
-  auto produce = [&](int q, const Cursor& cu) {
-    const int buf = q & 1;
-    const int j = cu.cb * JC + lane;
-    int m = 0, ws = 0, len = 0;
-    if (lane < JC && j < n_rx) {
-      m = g.rx_map[(int64_t)cu.e * n_rx + j];
-      const float t0 = t0s[cu.e];
-      ws = ((int)floorf(tmin[cu.e] + rmin[m] - t0) - 3) & ~3;
-      const int hi = (int)floorf(tmax[cu.e] + rmax[m] - t0) + 4;
-      len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
+  // staging metadata of running transmit T (all channels, all threads)
+  auto make_meta = [&](int T) {
+    const int e = T % n_tx;  // once per transmit, not per chunk
+    int2* M = meta + (T & 1) * n_rx;
+    const float t0 = t0s[e];
+    const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
+    const int* map = g.rx_map + (int64_t)e * n_rx;
+    for (int j = tid; j < n_rx; j += FTHREADS) {
+      const int m = map[j];
+      const int ws = ((int)floorf(lo_e + rmin[m]) - 3) & ~3;
+      const int hi = (int)floorf(hi_e + rmax[m]) + 4;
+      const int len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
+      M[j] = make_int2((m * FTHREADS * 8) | (len << 18), 4 * ws);
     }
-    const int v0 = max(ws, 0), v1 = min(ws + len, n_s);  // in-trace part
-    const uint32_t bytes = v1 > v0 ? (uint32_t)(v1 - v0) * 4u : 0u;
-    const uint32_t wb = win_s + (uint32_t)((buf * JC + lane) * W) * 4u;
-    if (lane < JC) {
-      float* wz = win + (buf * JC + lane) * W;
-      // zero sentinels for the part of the window outside the trace
-      for (int s0 = ws, e0 = min(v0, ws + len); s0 < e0; ++s0) wz[s0 - ws] = 0.0f;
-      for (int s0 = max(v1, ws); s0 < ws + len; ++s0) wz[s0 - ws] = 0.0f;
-      int* mo = reinterpret_cast<int*>(&meta[buf].pk[lane >> 1]) + 2 * (lane & 1);
-      mo[0] = m * FTHREADS * 8;
-      mo[1] = (int)(wb - (uint32_t)(kMagicBits + ws) * 4u);
-    }
-    uint32_t total = bytes;
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive_expect_tx(bar_s + 8 * buf, total);
-    if (bytes) {
-      const float* src = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
-                         ((int64_t)cu.e * n_rx + j) * n_s + v0;
-      bulk_g2s(wb + (uint32_t)(v0 - ws) * 4u, src, bytes, bar_s + 8 * buf);
+  };
+  // cp.async staging of chunk q: 4 threads per channel, 16 B per copy,
+  // zero fill (src-size 0) for 16 B groups outside the trace
+  auto issue_loads = [&](int q, const Cursor& cu) {
+    const int jj = tid >> 2;
+    const int j = cu.cb * JC + jj;
+    if (j >= n_rx) return;
+    const int2 mm = meta[(cu.T & 1) * n_rx + j];
+    const int ws = mm.y >> 2, len = (int)((unsigned)mm.x >> 18);
+    const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
+                      ((int64_t)cu.e * n_rx + j) * n_s;
+    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + jj) * W) * 4u;
+    for (int o = 4 * (tid & 3); o < len; o += 16) {
+      const int s0 = ws + o;
+      const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
+      cp_async16(wb + (uint32_t)o * 4u, in ? tr + s0 : tr, in ? 16 : 0);
     }
   };
 
-  Cursor cur{0, 0, 0}, nxt{0, 0, 0};
-  __syncthreads();  // barrier init visible to every thread
-  if (warp == 0) produce(0, nxt);
+  Cursor cur{0, 0, 0, 0}, nxt{0, 0, 0, 0};
+  make_meta(0);
+  __syncthreads();
+  issue_loads(0, nxt);
+  cp_async_commit();
   nxt.next(n_chunks, n_tx);
 
   const u64 M2 = pk(kMagic, kMagic);
@@ -278,9 +257,13 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
 
   for (int q = 0; q < Q; ++q) {
     __syncthreads();  // compute(q-1) done everywhere: buffer (q+1)&1 may be refilled
-    if (warp == 0 && q + 1 < Q) produce(q + 1, nxt);
+    if (cur.cb == 0 && cur.T + 1 < n_T) {
+      make_meta(cur.T + 1);  // ring slot of transmit T-1: all its loads/computes are done
+      __syncthreads();
+    }
+    if (q + 1 < Q) issue_loads(q + 1, nxt);
+    cp_async_commit();
     nxt.next(n_chunks, n_tx);
-
     if (cur.cb == 0) {
       if (PW) {
         const float ca = reinterpret_cast<const float*>(g.cos_a)[cur.e];
@@ -295,12 +278,16 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
       const float t0 = t0s[cur.e];
       t0e2 = pk(t0, t0);
     }
-    mbar_wait(bar_s + 8 * (q & 1), (uint32_t)((q >> 1) & 1));  // chunk q landed
+    cp_async_wait1();
+    __syncthreads();  // chunk q staged and visible
 
-    const ChunkMeta& M = meta[q & 1];
+    const int2* M = meta + (cur.T & 1) * n_rx + cur.cb * JC;
     const int jn = min(JC, n_rx - cur.cb * JC);
-    auto contrib = [&](int doff, int K) {
-      const u64 rxd = *reinterpret_cast<const u64*>(Dbytes + doff);
+    const uint32_t kb = win_s + (uint32_t)((q & 1) * JC * W) * 4u - (uint32_t)kMagicBits * 4u;
+    auto contrib = [&](int jj) {
+      const int2 mm = M[jj];
+      const uint32_t K = kb + (uint32_t)(jj * W) * 4u - (uint32_t)mm.y;
+      const u64 rxd = *reinterpret_cast<const u64*>(Dbytes + (mm.x & 0x3ffff));
       u64 t = add2(txd, rxd);
       if (T0) t = sub2(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
       if (LINEAR) {
@@ -308,32 +295,24 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
         const u64 k0f = add2(r, NM2);   // floor(t)
         const u64 fr = sub2(t, k0f);    // a = t - floor(t)
         const u64 om = sub2(ONE2, fr);  // 1 - a
-        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + (uint32_t)K;
-        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + (uint32_t)K;
+        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + K;
         const u64 x0 = pk(lds0(aA), lds0(aB));
         const u64 x1 = pk(lds1(aA), lds1(aB));
         acc = add2(acc, mul2(om, x0));  // acc = out + (1 - a) * x[k0]
         acc = add2(acc, mul2(fr, x1));  // out = acc + a * x[k1]
       } else {
         const u64 r = add2_rm(add2(t, HALF2), M2);  // floor(t + 0.5)
-        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + (uint32_t)K;
-        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + (uint32_t)K;
+        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + K;
         acc = add2(acc, pk(lds0(aA), lds0(aB)));
       }
     };
     if (jn == JC) {
 #pragma unroll
-      for (int jp = 0; jp < JC / 2; ++jp) {
-        const int4 mm = M.pk[jp];
-        contrib(mm.x, mm.y);
-        contrib(mm.z, mm.w);
-      }
+      for (int jj = 0; jj < JC; ++jj) contrib(jj);
     } else {
-      for (int jp = 0; jp < (jn + 1) / 2; ++jp) {
-        const int4 mm = M.pk[jp];
-        contrib(mm.x, mm.y);
-        if (2 * jp + 1 < jn) contrib(mm.z, mm.w);
-      }
+      for (int jj = 0; jj < jn; ++jj) contrib(jj);
     }
 
     if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
@@ -346,11 +325,12 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     }
     cur.next(n_chunks, n_tx);
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 size_t fast_smem_bytes(const bm_das_geometry& g, int W) {
   size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)(2 * g.n_elements + 2 * g.n_tx) * 4;
-  b = ((b + 15) & ~size_t(15)) + 2 * sizeof(ChunkMeta) + 2 * sizeof(uint64_t);
+  b = ((b + 15) & ~size_t(15)) + (size_t)2 * g.n_rx * 8;
   b = (b + 15) & ~size_t(15);
   return b + (size_t)2 * JC * W * 4;
 }
@@ -359,6 +339,7 @@ int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (fast_smem_bytes(g, g.window_hint) > 200 * 1024) return 0;
+  if (g.n_elements > 512 || g.window_hint >= (1 << 13)) return 0;  // meta packing
   return 1;
 }
 

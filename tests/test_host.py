@@ -144,4 +144,4 @@ def test_no_contracted_fma_in_das_kernels():
             if "FFMA2" in l:
                 assert "RZ" in l.split("FFMA2", 1)[1].split(";")[0], (n, l)
         assert any("FADD2.RM" in l for l in lines), n  # packed floor, magic constant
-        assert any("UBLKCP" in l for l in lines), n    # TMA bulk-copy staging
+        assert any("LDGSTS" in l for l in lines), n    # cp.async staging
