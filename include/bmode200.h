@@ -75,7 +75,7 @@ typedef struct bm_das_geometry {
                           window can span (0 = not prepared -> generic kernel) */
   int32_t t0_nonzero;  /* set by bm_das_prepare: 1 if any fs*t0 != 0 (the fast
                           kernel then keeps the reference's "- t0" rounding step) */
-  int32_t reserved;
+  int32_t rx_identity; /* set by bm_das_prepare: 1 if rx_map[e][j] == j for all e, j */
   double speed_of_sound;     /* c  (cast to dtype, beamform.py:206)          */
   double sampling_frequency; /* fs (cast to dtype, beamform.py:207)          */
   const double* elem_x;      /* [n_elements] element centres, f64            */
@@ -99,13 +99,15 @@ int bm_das_aperture_span(const bm_das_geometry* g, double f_number, int32_t* spa
                          void* stream);
 
 /* Host-side preparation of the fast (shared-memory-staged) DAS path: from
- * HOST copies of the element/grid positions and of fs*t0 (as double), bound
+ * HOST copies of the element/grid positions, of fs*t0 (as double) and of the
+ * [n_tx * n_rx] receive map, bound
  * the sample window any tile of the fast kernel can touch and check that all
  * delays stay in the exactly-representable range of its index arithmetic.
  * Writes g->window_hint (0 when the fast path does not apply).  Pure host
  * code: no device access, no stream. */
 int bm_das_prepare(bm_das_geometry* g, const double* elem_x_host, const double* x_host,
-                   const double* z_host, const double* t0_smp_host);
+                   const double* z_host, const double* t0_smp_host,
+                   const int32_t* rx_map_host);
 
 /* Delay-and-Sum of n_frames frames.
  *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride

@@ -31,7 +31,7 @@ class DasGeometry(ctypes.Structure):
         ("n_rx", ctypes.c_int32), ("n_samples", ctypes.c_int32),
         ("n_elements", ctypes.c_int32), ("n_z", ctypes.c_int32), ("n_x", ctypes.c_int32),
         ("window_hint", ctypes.c_int32), ("t0_nonzero", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("rx_identity", ctypes.c_int32),
         ("speed_of_sound", ctypes.c_double), ("sampling_frequency", ctypes.c_double),
         ("elem_x", ctypes.c_void_p), ("x_pos", ctypes.c_void_p), ("z_pos", ctypes.c_void_p),
         ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),
@@ -44,7 +44,7 @@ class DasGeometry(ctypes.Structure):
 _P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 SIGNATURES = {
     "bm_das_aperture_span": ([ctypes.POINTER(DasGeometry), _D, _P, _P], ctypes.c_int),
-    "bm_das_prepare": ([ctypes.POINTER(DasGeometry), _P, _P, _P, _P], ctypes.c_int),
+    "bm_das_prepare": ([ctypes.POINTER(DasGeometry), _P, _P, _P, _P, _P], ctypes.c_int),
     "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
     "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P], ctypes.c_int),
     "bm_envelope": ([_I32, _P, _P, _I64, _P], ctypes.c_int),

@@ -145,7 +145,7 @@ class DasPlan:
         he = np.ascontiguousarray(ctx.element_positions(), np.float64)
         ht = np.ascontiguousarray(t0_smp, np.float64)
         N.call("bm_das_prepare", ctypes.byref(g), he.ctypes.data, hx.ctypes.data,
-               hz.ctypes.data, ht.ctypes.data)
+               hz.ctypes.data, ht.ctypes.data, rx_map.ctypes.data)
         self.fast_window = int(g.window_hint)
         self._geom = g
         self.ctx, self.grid, self.apod, self.dtype, self.n_rx = ctx, grid, apod, dtype, n_rx

@@ -41,11 +41,21 @@ __device__ __forceinline__ u64 pk(float a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
   return r;
 }
+// split a packed pair into its two 32-bit halves (register-pair views, free)
+__device__ __forceinline__ void unpk(u64 r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
 __device__ __forceinline__ float lo_f(u64 r) {
-  return __uint_as_float((unsigned)(r & 0xffffffffu));
+  float a, b;
+  unpk(r, a, b);
+  (void)b;
+  return a;
 }
 __device__ __forceinline__ float hi_f(u64 r) {
-  return __uint_as_float((unsigned)(r >> 32));
+  float a, b;
+  unpk(r, a, b);
+  (void)a;
+  return b;
 }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   u64 d;
@@ -128,27 +138,30 @@ struct Cursor {
 };
 
 // Per-transmit staging metadata, one int2 per receive channel j:
-//   x = element m's D row byte offset (m * 64 threads * 8 B, < 2^18)
-//       | staged length (samples, multiple of 4, <= W) << 18,
-//   y = 4 * ws (first staged sample, a multiple of 4).
+//   x = staged length (samples, multiple of 4, <= W)
+//       | element m's D row byte offset (m * 64 threads * 8 B) << 13
+//         (IDMAP: the D row of channel j is row j, known at compile time),
+//   y = K, the shared-memory byte address of sample 0 of the channel's
+//       window minus 4 * (1.5*2^23 bits): x[k] lives at bits(floor(t)+M)*4 + K.
 // Ring of 2 transmits: meta(T + 1) is written at the first chunk of T.
-template <bool PW, bool LINEAR, bool T0>
+template <bool PW, bool LINEAR, bool T0, bool IDMAP>
 __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a) {
   using O = R<float>;
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
   const int W = a.W;
 
+  // shared memory carve-up (byte offsets from the shared base, so every
+  // access below stays an LDS/STS)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* D = reinterpret_cast<u64*>(smem_raw);                            // [n_el][64] pairs
-  float* rmin = reinterpret_cast<float*>(D + (size_t)n_el * FTHREADS);  // [n_el]
-  float* rmax = rmin + n_el;                                             // [n_el]
-  float* tmin = rmax + n_el;                                             // [n_tx]
-  float* tmax = tmin + n_tx;                                             // [n_tx]
-  int2* meta = reinterpret_cast<int2*>(
-      (reinterpret_cast<uintptr_t>(tmax + n_tx) + 15) & ~uintptr_t(15));  // [2][n_rx]
-  float* win = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(meta + 2 * n_rx) + 15) & ~uintptr_t(15));  // [2][JC][W]
+  const int off_tmin = n_el * FTHREADS * 8;
+  const int off_meta = (off_tmin + 8 * n_tx + 15) & ~15;
+  const int off_win = (off_meta + 16 * n_rx + 15) & ~15;
+  u64* D = reinterpret_cast<u64*>(smem_raw);                   // [n_el][64] pairs
+  float* tmin = reinterpret_cast<float*>(smem_raw + off_tmin);  // [n_tx]
+  float* tmax = tmin + n_tx;                                    // [n_tx]
+  int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [2][n_rx]
+  float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [2][JC][W]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -176,14 +189,15 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + FX, g.n_x) - 1];
   const double z0 = g.z_pos[tz0], z1 = g.z_pos[min(tz0 + FZ, g.n_z) - 1];
   const double k = g.sampling_frequency / g.speed_of_sound;
-  for (int m = tid; m < n_el; m += FTHREADS) {
+  // receive-path delay bounds of element m over the tile rectangle: nearest
+  // and farthest point, in samples
+  auto rx_bounds = [&](int m, float& lo, float& hi) {
     const double xm = g.elem_x[m];
     const double dmin = fmax(0.0, fmax(x0 - xm, xm - x1));
     const double dmax = fmax(fabs(x0 - xm), fabs(x1 - xm));
-    rmin[m] = (float)(k * sqrt(dmin * dmin + z0 * z0));
-    rmax[m] = (float)(k * sqrt(dmax * dmax + z1 * z1));
-  }
-  __syncthreads();
+    lo = (float)(k * sqrt(dmin * dmin + z0 * z0));
+    hi = (float)(k * sqrt(dmax * dmax + z1 * z1));
+  };
   for (int e = tid; e < n_tx; e += FTHREADS) {
     if (PW) {
       const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
@@ -193,9 +207,7 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
       tmin[e] = (float)(k * fmin(fmin(v00, v01), fmin(v10, v11)));
       tmax[e] = (float)(k * fmax(fmax(v00, v01), fmax(v10, v11)));
     } else {
-      const int te = g.tx_elements[e];
-      tmin[e] = rmin[te];
-      tmax[e] = rmax[te];
+      rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
     }
   }
   __syncthreads();
@@ -207,7 +219,9 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
   const int Q = f_count * n_tx * n_chunks;
   const int n_T = f_count * n_tx;
 
-  // staging metadata of running transmit T (all channels, all threads)
+  // staging metadata of running transmit T (all channels, all threads).
+  // Chunk q of transmit T is q = T * n_chunks + cb, so its window buffer
+  // (q & 1) -- and with it K -- is known here.
   auto make_meta = [&](int T) {
     const int e = T % n_tx;  // once per transmit, not per chunk
     int2* M = meta + (T & 1) * n_rx;
@@ -215,11 +229,17 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
     const int* map = g.rx_map + (int64_t)e * n_rx;
     for (int j = tid; j < n_rx; j += FTHREADS) {
-      const int m = map[j];
-      const int ws = ((int)floorf(lo_e + rmin[m]) - 3) & ~3;
-      const int hi = (int)floorf(hi_e + rmax[m]) + 4;
+      const int m = IDMAP ? j : map[j];
+      float rlo, rhi;
+      rx_bounds(m, rlo, rhi);
+      const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
+      const int hi = (int)floorf(hi_e + rhi) + 4;
       const int len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
-      M[j] = make_int2((m * FTHREADS * 8) | (len << 18), 4 * ws);
+      const int cb = j / JC, jj = j - cb * JC;
+      const int buf = (T * n_chunks + cb) & 1;
+      const uint32_t K = win_s + (uint32_t)((buf * JC + jj) * W) * 4u -
+                         (uint32_t)(kMagicBits + ws) * 4u;
+      M[j] = make_int2(len | ((m * FTHREADS * 8) << 13), (int)K);
     }
   };
   // cp.async staging of chunk q: 4 threads per channel, 16 B per copy,
@@ -229,10 +249,11 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     const int j = cu.cb * JC + jj;
     if (j >= n_rx) return;
     const int2 mm = meta[(cu.T & 1) * n_rx + j];
-    const int ws = mm.y >> 2, len = (int)((unsigned)mm.x >> 18);
+    const int len = mm.x & 0x1fff;
+    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + jj) * W) * 4u;
+    const int ws = (int)((wb - (uint32_t)mm.y) >> 2) - kMagicBits;
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + j) * n_s;
-    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + jj) * W) * 4u;
     for (int o = 4 * (tid & 3); o < len; o += 16) {
       const int s0 = ws + o;
       const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
@@ -283,11 +304,12 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
 
     const int2* M = meta + (cur.T & 1) * n_rx + cur.cb * JC;
     const int jn = min(JC, n_rx - cur.cb * JC);
-    const uint32_t kb = win_s + (uint32_t)((q & 1) * JC * W) * 4u - (uint32_t)kMagicBits * 4u;
+    const unsigned char* Dchunk = Dbytes + cur.cb * JC * FTHREADS * 8;
     auto contrib = [&](int jj) {
       const int2 mm = M[jj];
-      const uint32_t K = kb + (uint32_t)(jj * W) * 4u - (uint32_t)mm.y;
-      const u64 rxd = *reinterpret_cast<const u64*>(Dbytes + (mm.x & 0x3ffff));
+      const uint32_t K = (uint32_t)mm.y;
+      const u64 rxd = IDMAP ? *reinterpret_cast<const u64*>(Dchunk + jj * FTHREADS * 8)
+                            : *reinterpret_cast<const u64*>(Dbytes + ((unsigned)mm.x >> 13));
       u64 t = add2(txd, rxd);
       if (T0) t = sub2(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
       if (LINEAR) {
@@ -295,16 +317,20 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
         const u64 k0f = add2(r, NM2);   // floor(t)
         const u64 fr = sub2(t, k0f);    // a = t - floor(t)
         const u64 om = sub2(ONE2, fr);  // 1 - a
-        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + K;
-        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + K;
+        float rA, rB;
+        unpk(r, rA, rB);
+        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
         const u64 x0 = pk(lds0(aA), lds0(aB));
         const u64 x1 = pk(lds1(aA), lds1(aB));
         acc = add2(acc, mul2(om, x0));  // acc = out + (1 - a) * x[k0]
         acc = add2(acc, mul2(fr, x1));  // out = acc + a * x[k1]
       } else {
         const u64 r = add2_rm(add2(t, HALF2), M2);  // floor(t + 0.5)
-        const uint32_t aA = (uint32_t)__float_as_int(lo_f(r)) * 4u + K;
-        const uint32_t aB = (uint32_t)__float_as_int(hi_f(r)) * 4u + K;
+        float rA, rB;
+        unpk(r, rA, rB);
+        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
         acc = add2(acc, pk(lds0(aA), lds0(aB)));
       }
     };
@@ -329,8 +355,8 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
 }
 
 size_t fast_smem_bytes(const bm_das_geometry& g, int W) {
-  size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)(2 * g.n_elements + 2 * g.n_tx) * 4;
-  b = ((b + 15) & ~size_t(15)) + (size_t)2 * g.n_rx * 8;
+  size_t b = (size_t)g.n_elements * FTHREADS * 8 + (size_t)g.n_tx * 8;
+  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 16;
   b = (b + 15) & ~size_t(15);
   return b + (size_t)2 * JC * W * 4;
 }
@@ -339,7 +365,7 @@ int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (fast_smem_bytes(g, g.window_hint) > 200 * 1024) return 0;
-  if (g.n_elements > 512 || g.window_hint >= (1 << 13)) return 0;  // meta packing
+  if (g.n_elements > 512 || g.window_hint >= (1 << 13)) return 0;  // meta packing (19 + 13 bits)
   return 1;
 }
 
@@ -356,13 +382,19 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   a.frames_per_cta = fpc;
   const size_t smem = fast_smem_bytes(g, a.W);
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
-  decltype(&das_fast_kernel<true, true, true>) k;
-  if (g.t0_nonzero)
-    k = pw ? (lin ? das_fast_kernel<true, true, true> : das_fast_kernel<true, false, true>)
-           : (lin ? das_fast_kernel<false, true, true> : das_fast_kernel<false, false, true>);
-  else
-    k = pw ? (lin ? das_fast_kernel<true, true, false> : das_fast_kernel<true, false, false>)
-           : (lin ? das_fast_kernel<false, true, false> : das_fast_kernel<false, false, false>);
+  typedef void (*kfn)(const FastArgs);
+  // [pw][lin][t0][idmap]
+  static const kfn table[16] = {
+      das_fast_kernel<false, false, false, false>, das_fast_kernel<false, false, false, true>,
+      das_fast_kernel<false, false, true, false>,  das_fast_kernel<false, false, true, true>,
+      das_fast_kernel<false, true, false, false>,  das_fast_kernel<false, true, false, true>,
+      das_fast_kernel<false, true, true, false>,   das_fast_kernel<false, true, true, true>,
+      das_fast_kernel<true, false, false, false>,  das_fast_kernel<true, false, false, true>,
+      das_fast_kernel<true, false, true, false>,   das_fast_kernel<true, false, true, true>,
+      das_fast_kernel<true, true, false, false>,   das_fast_kernel<true, true, false, true>,
+      das_fast_kernel<true, true, true, false>,    das_fast_kernel<true, true, true, true>};
+  const kfn k = table[(pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
+                      (g.rx_identity ? 1 : 0)];
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
@@ -374,10 +406,11 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
 
 // Host-only: bound the fast kernel's per-(e, j) sample window over all tiles.
 extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const double* x,
-                              const double* z, const double* t0_smp) {
-  if (!g || !elem_x || !x || !z || !t0_smp) return BM_ERR_INVALID_ARGUMENT;
+                              const double* z, const double* t0_smp, const int32_t* rx_map) {
+  if (!g || !elem_x || !x || !z || !t0_smp || !rx_map) return BM_ERR_INVALID_ARGUMENT;
   g->window_hint = 0;
   g->t0_nonzero = 1;
+  g->rx_identity = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   double zext = 0.0, xext = 0.0;
   for (int i = 0; i < g->n_z; i += bm::FZ) {
@@ -411,6 +444,10 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
     if (t0_smp[e] != 0.0) g->t0_nonzero = 1;
   }
   const double tabs = 2.0 * k * dmax + t0max + 16.0 + W;
+  int ident = g->n_rx <= g->n_elements;
+  for (int64_t i = 0; ident && i < (int64_t)g->n_tx * g->n_rx; ++i)
+    if (rx_map[i] != (int)(i % g->n_rx)) ident = 0;
+  g->rx_identity = ident;
   if (!(tabs < 4194304.0)) return BM_OK;  // outside the exact magic-number range
   if (W > 4096) return BM_OK;
   g->window_hint = W;
