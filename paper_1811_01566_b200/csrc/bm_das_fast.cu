@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     const int2 mm = meta[(cu.T & 1) * n_rx + j];
     const int len = mm.x & 0x1fff;
     const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + jj) * W) * 4u;
-    const int ws = (int)((wb - (uint32_t)mm.y) >> 2) - kMagicBits;
+    // K = wb - 4*(M_bits + ws) mod 2^32, so (wb - K)/4 = (M_bits + ws) mod 2^30
+    const int ws = (int)((wb - (uint32_t)mm.y) >> 2) - (kMagicBits & 0x3fffffff);
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + j) * n_s;
     for (int o = 4 * (tid & 3); o < len; o += 16) {
