@@ -243,22 +243,31 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     }
   };
   // cp.async staging of chunk q: 4 threads per channel, 16 B per copy,
-  // zero fill (src-size 0) for 16 B groups outside the trace
+  // zero fill (src-size 0) for 16 B groups outside the trace.  Thread tid
+  // always serves channel jj = tid / 4 of a chunk and copy slots
+  // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 4 (host guarantees W <= 64
+  // for this kernel), so the per-chunk work is a few adds.
+  const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
+  const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
   auto issue_loads = [&](int q, const Cursor& cu) {
-    const int jj = tid >> 2;
-    const int j = cu.cb * JC + jj;
+    const int j = cu.cb * JC + ld_jj;
     if (j >= n_rx) return;
     const int2 mm = meta[(cu.T & 1) * n_rx + j];
     const int len = mm.x & 0x1fff;
-    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + jj) * W) * 4u;
-    // K = wb - 4*(M_bits + ws) mod 2^32, so (wb - K)/4 = (M_bits + ws) mod 2^30
-    const int ws = (int)((wb - (uint32_t)mm.y) >> 2) - (kMagicBits & 0x3fffffff);
+    const uint32_t wb = win_s + (uint32_t)(((q & 1) * JC + ld_jj) * W + ld_o) * 4u;
+    // K = wb0 - 4*(M_bits + ws) mod 2^32, so (wb0 - K)/4 = (M_bits + ws) mod 2^30
+    const int ws = (int)((wb - (uint32_t)ld_o * 4u - (uint32_t)mm.y) >> 2) -
+                   (kMagicBits & 0x3fffffff);
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
-                      ((int64_t)cu.e * n_rx + j) * n_s;
-    for (int o = 4 * (tid & 3); o < len; o += 16) {
-      const int s0 = ws + o;
-      const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
-      cp_async16(wb + (uint32_t)o * 4u, in ? tr + s0 : tr, in ? 16 : 0);
+                      ((int64_t)cu.e * n_rx + cu.cb * JC) * n_s + ld_trace;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int o = ld_o + 16 * i;
+      if (o < len) {
+        const int s0 = ws + o;
+        const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
+        cp_async16(wb + 64u * i, tr + (in ? ws + 16 * i : -ld_o), in ? 16 : 0);
+      }
     }
   };
 
@@ -366,7 +375,8 @@ int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (fast_smem_bytes(g, g.window_hint) > 200 * 1024) return 0;
-  if (g.n_elements > 512 || g.window_hint >= (1 << 13)) return 0;  // meta packing (19 + 13 bits)
+  if (g.n_elements > 512) return 0;  // meta packing: D offset in 19 bits
+  if (g.window_hint > 64) return 0;  // loader: <= 4 copies of 16 B per thread
   return 1;
 }
 
