@@ -344,9 +344,47 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
         acc = add2(acc, pk(lds0(aA), lds0(aB)));
       }
     };
+    // Full chunks run in groups of G channels, each stage issued for the whole
+    // group before the next (delays, then floors and gather addresses, then
+    // the shared-memory gathers, then the arithmetic and the in-order
+    // accumulation), so every warp keeps G independent gathers in flight.
+    constexpr int G = 8;
+    auto group = [&](int j0) {
+      u64 t[G], r[G], x0[G], x1[G];
+      uint32_t aA[G], aB[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const int2 mm = M[j0 + i];
+        const u64 rxd = IDMAP ? *reinterpret_cast<const u64*>(Dchunk + (j0 + i) * FTHREADS * 8)
+                              : *reinterpret_cast<const u64*>(Dbytes + ((unsigned)mm.x >> 13));
+        t[i] = add2(txd, rxd);
+        if (T0) t[i] = sub2(t[i], t0e2);
+        r[i] = LINEAR ? add2_rm(t[i], M2) : add2_rm(add2(t[i], HALF2), M2);
+        float rA, rB;
+        unpk(r[i], rA, rB);
+        aA[i] = (uint32_t)__float_as_int(rA) * 4u + (uint32_t)mm.y;
+        aB[i] = (uint32_t)__float_as_int(rB) * 4u + (uint32_t)mm.y;
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        x0[i] = pk(lds0(aA[i]), lds0(aB[i]));
+        if (LINEAR) x1[i] = pk(lds1(aA[i]), lds1(aB[i]));
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (LINEAR) {
+          const u64 fr = sub2(t[i], add2(r[i], NM2));  // a = t - floor(t)
+          const u64 om = sub2(ONE2, fr);               // 1 - a
+          acc = add2(acc, mul2(om, x0[i]));            // acc = out + (1 - a) * x[k0]
+          acc = add2(acc, mul2(fr, x1[i]));            // out = acc + a * x[k1]
+        } else {
+          acc = add2(acc, x0[i]);
+        }
+      }
+    };
     if (jn == JC) {
 #pragma unroll
-      for (int jj = 0; jj < JC; ++jj) contrib(jj);
+      for (int j0 = 0; j0 < JC; j0 += G) group(j0);
     } else {
       for (int jj = 0; jj < jn; ++jj) contrib(jj);
     }
