@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "../../include/bmode200.h"
 
@@ -46,9 +48,26 @@ inline int sm_count() {
   return n;
 }
 
-// fast (shared-memory-staged, f32x2) DAS path, bm_das_fast.cu
+// fast (shared-memory-staged, f32x2) DAS paths: delay table in shared
+// memory (bm_das_fast.cu) or in tensor memory (bm_das_tmem.cu)
 int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                     int64_t out_stride, int n_frames, cudaStream_t s);
+int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride);
+int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                    int64_t out_stride, int n_frames, cudaStream_t s);
+
+// DAS kernel selection: BM_DAS_KERNEL = auto (default) | tmem | smem | generic
+inline int das_kernel_choice() {
+  static int choice = -1;
+  if (choice < 0) {
+    const char* e = getenv("BM_DAS_KERNEL");
+    choice = 0;
+    if (e && !strcmp(e, "tmem")) choice = 1;
+    if (e && !strcmp(e, "smem")) choice = 2;
+    if (e && !strcmp(e, "generic")) choice = 3;
+  }
+  return choice;
+}
 
 }  // namespace bm

@@ -241,7 +241,10 @@ extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t
   if (!rf || !out || n_frames < 0 || n_frames > 65535) return BM_ERR_INVALID_ARGUMENT;
   if (n_frames == 0) return BM_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (bm::das_fast_eligible(*g, rf_frame_stride))
+  const int choice = bm::das_kernel_choice();
+  if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
+    return bm::das_tmem_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
+  if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride))
     return bm::das_fast_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
   bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride};
   if (g->dtype == BM_F32)

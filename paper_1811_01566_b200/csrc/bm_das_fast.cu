@@ -26,67 +26,11 @@
 //  * floor(t) and the integer sample index come from one FADD2.RM with the
 //    1.5*2^23 magic constant (exact for |t| < 2^22, checked on the host by
 //    bm_das_prepare); the index is the float's bit pattern, so no F2I.
-#include "bm_common.cuh"
+#include "bm_f32x2.cuh"
 
 namespace bm {
 
 constexpr int FZ = 8, FX = 16, FTHREADS = 64, JC = 16;
-constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-constexpr int kMagicBits = 0x4B400000;
-
-typedef unsigned long long u64;
-
-__device__ __forceinline__ u64 pk(float a, float b) {
-  u64 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-// split a packed pair into its two 32-bit halves (register-pair views, free)
-__device__ __forceinline__ void unpk(u64 r, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ float lo_f(u64 r) {
-  float a, b;
-  unpk(r, a, b);
-  (void)b;
-  return a;
-}
-__device__ __forceinline__ float hi_f(u64 r) {
-  float a, b;
-  unpk(r, a, b);
-  (void)a;
-  return b;
-}
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ u64 add2_rm(u64 a, u64 b) {
-  u64 d;
-  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-// Product rounded once, as a separate operation.  ptxas (CUDA 12.9) contracts
-// mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 even under --fmad=false,
-// which would drop the product's rounding (the reference rounds it:
-// beamform.py:178-187).  fma(a, b, +0) = RN(a*b) is not contracted further;
-// it differs from mul only in the sign of an exact-zero product, which cannot
-// change the running sum (the accumulator starts at +0 and, in round-to-
-// nearest, can never become -0, and x + (+-0) == x for every other x).
-// tests/test_host.py::test_no_contracted_fma_in_das_kernels checks the SASS.
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(0ull));
-  return d;
-}
-
-
 struct FastArgs {
   bm_das_geometry g;
   const float* rf;
@@ -96,45 +40,6 @@ struct FastArgs {
   int n_frames;
   int frames_per_cta;
   int W;  // staged window capacity per channel (samples, multiple of 4)
-};
-
-__device__ __forceinline__ float lds0(uint32_t a) {
-  float v;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ float lds1(uint32_t a) {
-  float v;
-  asm("ld.shared.f32 %0, [%1+4];" : "=f"(v) : "r"(a));
-  return v;
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr), "l"(gptr),
-               "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait1() {
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-}
-
-// Chunk cursor: q -> (frame in group, transmit e, channel block cb), advanced
-// incrementally (no integer division in the loop).  T = fl * n_tx + e.
-struct Cursor {
-  int fl, e, cb, T;
-  __device__ __forceinline__ void next(int n_chunks, int n_tx) {
-    if (++cb == n_chunks) {
-      cb = 0;
-      ++T;
-      if (++e == n_tx) {
-        e = 0;
-        ++fl;
-      }
-    }
-  }
 };
 
 // Per-transmit staging metadata, one int2 per receive channel j:
@@ -261,7 +166,7 @@ __global__ void __launch_bounds__(FTHREADS, 3) das_fast_kernel(const FastArgs a)
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + cu.cb * JC) * n_s + ld_trace;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const int o = ld_o + 16 * i;
       if (o < len) {
         const int s0 = ws + o;
@@ -414,7 +319,7 @@ int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (fast_smem_bytes(g, g.window_hint) > 200 * 1024) return 0;
   if (g.n_elements > 512) return 0;  // meta packing: D offset in 19 bits
-  if (g.window_hint > 64) return 0;  // loader: <= 4 copies of 16 B per thread
+  if (g.window_hint > 128) return 0;  // loader: <= 8 copies of 16 B per thread
   return 1;
 }
 
@@ -462,12 +367,14 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->rx_identity = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   double zext = 0.0, xext = 0.0;
-  for (int i = 0; i < g->n_z; i += bm::FZ) {
-    const int l = (i + bm::FZ < g->n_z ? i + bm::FZ : g->n_z) - 1;
+  // the largest tile of either fast kernel (16 x 16 pixels) bounds both
+  const int TZM = 16, TXM = 16;
+  for (int i = 0; i < g->n_z; i += TZM) {
+    const int l = (i + TZM < g->n_z ? i + TZM : g->n_z) - 1;
     zext = fmax(zext, z[l] - z[i]);
   }
-  for (int i = 0; i < g->n_x; i += bm::FX) {
-    const int l = (i + bm::FX < g->n_x ? i + bm::FX : g->n_x) - 1;
+  for (int i = 0; i < g->n_x; i += TXM) {
+    const int l = (i + TXM < g->n_x ? i + TXM : g->n_x) - 1;
     xext = fmax(xext, x[l] - x[i]);
   }
   const double k = g->sampling_frequency / g->speed_of_sound;

@@ -1,0 +1,395 @@
+// K1 fast path with the receive-delay table in TENSOR MEMORY (sm_100a).
+//
+// Same arithmetic (and therefore the same bits) as das_fast_kernel and the
+// reference's f32 das_beamform (beamform.py:122-187 with the DasPlan delays
+// of :211-228).  The difference is where the per-tile delay table
+// D[m][pixel] = fs*(sqrt(dx^2+z^2)/c) lives:
+//
+//  * The shared-memory kernel keeps D in SMEM (n_el x 8 B per thread), which
+//    caps residency at 3 CTAs x 2 warps per SM and costs one LDS.64 and one
+//    shared-memory wavefront per channel.
+//  * Here D lives in TMEM, the 256 KB per-SM tensor memory that no other part
+//    of this kernel uses: thread (warp w, lane l) owns TMEM lane 32w + l and
+//    the two columns 2m, 2m+1 hold its pixel pair's delays to element m.  A
+//    chunk of 16 channels is ONE tcgen05.ld.32x32b.x32 into registers, and
+//    shared memory is left to the RF windows -- 2 CTAs x 4 warps per SM.
+//
+// CTA = 128 threads, tile = 16 rows x 16 columns; warp w covers an 8 x 8
+// block (columns 8*(w&1).., rows 8*(w>>1)..), lane l the pixel pair
+// (row l/8, col l%8) / (row l/8 + 4, col l%8), so each gather of a warp is a
+// 4 x 8 pixel block (conflict-free, see das_fast_kernel).  RF windows are
+// staged per chunk of 32 channels with cp.async exactly as in
+// das_fast_kernel.
+#include "bm_f32x2.cuh"
+
+namespace bm {
+
+constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 32;
+
+struct TmemArgs {
+  bm_das_geometry g;
+  const float* rf;
+  int64_t rf_stride;
+  float* out;
+  int64_t out_stride;
+  int n_frames;
+  int frames_per_cta;
+  int W;          // staged window capacity per channel (samples, multiple of 4)
+  int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
+};
+
+// ---- tcgen05 (TMEM) helpers
+__device__ __forceinline__ void tm_alloc(uint32_t smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tm_relinquish() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tm_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, float a, float b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "f"(a), "f"(b)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// x2 load + wait; the wait takes the destinations as in-out operands so no
+// use of them can be scheduled before the load has landed.
+__device__ __forceinline__ u64 tm_ld2(uint32_t taddr) {
+  uint32_t a, b;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
+  return ((u64)b << 32) | a;
+}
+// 16 channel pairs (32 columns) in one instruction
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, u64 (&d)[16]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])::"memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d[i] = ((u64)r[2 * i + 1] << 32) | r[2 * i];
+}
+
+template <bool PW, bool LINEAR, bool T0, bool IDMAP>
+__global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a) {
+  using O = R<float>;
+  const bm_das_geometry& g = a.g;
+  const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
+  const int W = a.W;
+
+  // shared memory: [tmem base][tmin|tmax][meta ring][windows]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int off_tmin = 16;
+  const int off_meta = (off_tmin + 8 * n_tx + 15) & ~15;
+  const int off_win = (off_meta + 16 * n_rx + 15) & ~15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
+  float* tmin = reinterpret_cast<float*>(smem_raw + off_tmin);  // [n_tx]
+  float* tmax = tmin + n_tx;                                    // [n_tx]
+  int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [2][n_rx]
+  float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [2][TJC][W]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int tiles_x = (g.n_x + TX - 1) / TX;
+  const int tz0 = (blockIdx.x / tiles_x) * TZ, tx0 = (blockIdx.x % tiles_x) * TX;
+  const int col = tx0 + (warp & 1) * 8 + (lane & 7);
+  const int rowA = tz0 + (warp >> 1) * 8 + (lane >> 3), rowB = rowA + 4;
+  const int colc = min(col, g.n_x - 1);
+  const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
+
+  const float c = O::from_double(g.speed_of_sound);
+  const float fs = O::from_double(g.sampling_frequency);
+  const double px = g.x_pos[colc];
+  const float pxd = O::from_double(px);
+  const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
+
+  // ---- TMEM allocation (warp 0), address broadcast through shared memory
+  if (warp == 0) {
+    tm_alloc((uint32_t)__cvta_generic_to_shared(tmem_slot), (uint32_t)a.tmem_cols);
+    tm_relinquish();
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
+
+  // ---- exact receive delays of the pixel pair -> TMEM columns 2m, 2m+1
+  for (int m = 0; m < n_el; ++m) {
+    const float dx = O::from_double(g.elem_x[m] - px);
+    const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
+    const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
+    tm_st2(tlane + 2 * m, dA, dB);
+  }
+  tm_wait_st();
+
+  const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TX, g.n_x) - 1];
+  const double z0 = g.z_pos[tz0], z1 = g.z_pos[min(tz0 + TZ, g.n_z) - 1];
+  const double k = g.sampling_frequency / g.speed_of_sound;
+  // receive-path delay bounds of element m over the tile rectangle (samples)
+  auto rx_bounds = [&](int m, float& lo, float& hi) {
+    const double xm = g.elem_x[m];
+    const double dmin = fmax(0.0, fmax(x0 - xm, xm - x1));
+    const double dmax = fmax(fabs(x0 - xm), fabs(x1 - xm));
+    lo = (float)(k * sqrt(dmin * dmin + z0 * z0));
+    hi = (float)(k * sqrt(dmax * dmax + z1 * z1));
+  };
+  for (int e = tid; e < n_tx; e += TTHREADS) {
+    if (PW) {
+      const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
+      const double sa = reinterpret_cast<const float*>(g.sin_a)[e];
+      const double v00 = z0 * ca + x0 * sa, v01 = z0 * ca + x1 * sa;
+      const double v10 = z1 * ca + x0 * sa, v11 = z1 * ca + x1 * sa;
+      tmin[e] = (float)(k * fmin(fmin(v00, v01), fmin(v10, v11)));
+      tmax[e] = (float)(k * fmax(fmax(v00, v01), fmax(v10, v11)));
+    } else {
+      rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
+    }
+  }
+  __syncthreads();
+
+  const float* __restrict__ t0s = reinterpret_cast<const float*>(g.t0_smp);
+  const int n_chunks = (n_rx + TJC - 1) / TJC;
+  const int f_begin = blockIdx.y * a.frames_per_cta;
+  const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
+  const int Q = f_count * n_tx * n_chunks;
+  const int n_T = f_count * n_tx;
+
+  // staging metadata of running transmit T: per channel
+  //   x = staged length | element m << 13,  y = K (gather address base)
+  auto make_meta = [&](int T) {
+    const int e = T % n_tx;
+    int2* M = meta + (T & 1) * n_rx;
+    const float t0 = t0s[e];
+    const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
+    const int* map = g.rx_map + (int64_t)e * n_rx;
+    for (int j = tid; j < n_rx; j += TTHREADS) {
+      const int m = IDMAP ? j : map[j];
+      float rlo, rhi;
+      rx_bounds(m, rlo, rhi);
+      const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
+      const int hi = (int)floorf(hi_e + rhi) + 4;
+      const int len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
+      const int cb = j / TJC, jj = j - cb * TJC;
+      const int buf = (T * n_chunks + cb) & 1;
+      const uint32_t K = win_s + (uint32_t)((buf * TJC + jj) * W) * 4u -
+                         (uint32_t)(kMagicBits + ws) * 4u;
+      M[j] = make_int2(len | (m << 13), (int)K);
+    }
+  };
+  // cp.async staging: 4 threads per channel, 16 B copies at fixed slots
+  const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
+  const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
+  auto issue_loads = [&](int q, const Cursor& cu) {
+    const int j = cu.cb * TJC + ld_jj;
+    if (j >= n_rx) return;
+    const int2 mm = meta[(cu.T & 1) * n_rx + j];
+    const int len = mm.x & 0x1fff;
+    const uint32_t wb = win_s + (uint32_t)(((q & 1) * TJC + ld_jj) * W + ld_o) * 4u;
+    // K = wb0 - 4*(M_bits + ws) mod 2^32, so (wb0 - K)/4 = (M_bits + ws) mod 2^30
+    const int ws = (int)((wb - (uint32_t)ld_o * 4u - (uint32_t)mm.y) >> 2) -
+                   (kMagicBits & 0x3fffffff);
+    const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
+                      ((int64_t)cu.e * n_rx + cu.cb * TJC) * n_s + ld_trace;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int o = ld_o + 16 * i;
+      if (o < len) {
+        const int s0 = ws + o;
+        const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
+        cp_async16(wb + 64u * i, tr + (in ? ws + 16 * i : -ld_o), in ? 16 : 0);
+      }
+    }
+  };
+
+  Cursor cur{0, 0, 0, 0}, nxt{0, 0, 0, 0};
+  make_meta(0);
+  __syncthreads();
+  issue_loads(0, nxt);
+  cp_async_commit();
+  nxt.next(n_chunks, n_tx);
+
+  const u64 M2 = pk(kMagic, kMagic);
+  const u64 NM2 = pk(-kMagic, -kMagic);
+  const u64 ONE2 = pk(1.0f, 1.0f);
+  const u64 HALF2 = pk(0.5f, 0.5f);
+  u64 acc = 0ull;  // (+0.0f, +0.0f)
+  u64 txd = 0ull, t0e2 = 0ull;
+
+  for (int q = 0; q < Q; ++q) {
+    __syncthreads();  // compute(q-1) done everywhere: buffer (q+1)&1 may be refilled
+    if (cur.cb == 0 && cur.T + 1 < n_T) {
+      make_meta(cur.T + 1);  // ring slot of transmit T-1: all its loads/computes are done
+      __syncthreads();
+    }
+    if (q + 1 < Q) issue_loads(q + 1, nxt);
+    cp_async_commit();
+    nxt.next(n_chunks, n_tx);
+    if (cur.cb == 0) {
+      if (PW) {
+        const float ca = reinterpret_cast<const float*>(g.cos_a)[cur.e];
+        const float sa = reinterpret_cast<const float*>(g.sin_a)[cur.e];
+        const float xs = O::mul(pxd, sa);
+        const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+        const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
+        txd = pk(tA, tB);
+      } else {
+        txd = tm_ld2(tlane + 2 * g.tx_elements[cur.e]);
+      }
+      const float t0 = t0s[cur.e];
+      t0e2 = pk(t0, t0);
+    }
+    cp_async_wait1();
+    __syncthreads();  // chunk q staged and visible
+
+    const int2* M = meta + (cur.T & 1) * n_rx + cur.cb * TJC;
+    const int jn = min(TJC, n_rx - cur.cb * TJC);
+
+    // one channel: rxd = receive delays of the pair, mm = staging metadata
+    auto channel = [&](u64 rxd, int2 mm) {
+      u64 t = add2(txd, rxd);
+      if (T0) t = sub2(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
+      const uint32_t K = (uint32_t)mm.y;
+      if (LINEAR) {
+        const u64 r = add2_rm(t, M2);   // floor(t) + 1.5*2^23, exactly
+        float rA, rB;
+        unpk(r, rA, rB);
+        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
+        const u64 x0 = pk(lds0(aA), lds0(aB));
+        const u64 x1 = pk(lds1(aA), lds1(aB));
+        const u64 fr = sub2(t, add2(r, NM2));  // a = t - floor(t)
+        const u64 om = sub2(ONE2, fr);         // 1 - a
+        acc = add2(acc, mul2(om, x0));         // acc = out + (1 - a) * x[k0]
+        acc = add2(acc, mul2(fr, x1));         // out = acc + a * x[k1]
+      } else {
+        const u64 r = add2_rm(add2(t, HALF2), M2);  // floor(t + 0.5)
+        float rA, rB;
+        unpk(r, rA, rB);
+        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
+        acc = add2(acc, pk(lds0(aA), lds0(aB)));
+      }
+    };
+    if (IDMAP && jn == TJC) {
+      // identity map: channels cb*32 .. cb*32+31 are elements of the same
+      // index -- two tcgen05.ld.x32 fetch all 32 delay pairs
+#pragma unroll
+      for (int h = 0; h < TJC; h += 16) {
+        u64 d[16];
+        tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) channel(d[i], M[h + i]);
+      }
+    } else {
+      for (int jj = 0; jj < jn; ++jj) {
+        const int2 mm = M[jj];
+        channel(tm_ld2(tlane + 2 * ((unsigned)mm.x >> 13)), mm);
+      }
+    }
+
+    if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
+      const int64_t fo = (int64_t)(f_begin + cur.fl) * a.out_stride;
+      if (col < g.n_x) {
+        if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = lo_f(acc);
+        if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = hi_f(acc);
+      }
+      acc = 0ull;
+    }
+    cur.next(n_chunks, n_tx);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+
+  // ---- release TMEM (the allocating warp)
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  if (warp == 0) tm_dealloc(tbase, (uint32_t)a.tmem_cols);
+}
+
+static size_t tmem_smem_bytes(const bm_das_geometry& g, int W) {
+  size_t b = 16 + (size_t)g.n_tx * 8;
+  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 16;
+  b = (b + 15) & ~size_t(15);
+  return b + (size_t)2 * TJC * W * 4;
+}
+
+static int tmem_cols_for(int n_el) {
+  int cols = 32;
+  while (cols < 2 * n_el) cols *= 2;
+  return cols;
+}
+
+int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride) {
+  if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
+  if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
+  if (g.window_hint > 128) return 0;              // loader: <= 8 copies of 16 B per thread
+  if (2 * g.n_elements > 512) return 0;          // one TMEM column pair per element
+  if (tmem_smem_bytes(g, g.window_hint) > 110 * 1024) return 0;
+  return 1;
+}
+
+int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                    int64_t out_stride, int n_frames, cudaStream_t s) {
+  TmemArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1,
+             g.window_hint, tmem_cols_for(g.n_elements)};
+  const int tiles = ((g.n_z + TZ - 1) / TZ) * ((g.n_x + TX - 1) / TX);
+  // CTAs per SM are limited to what TMEM holds (512 columns): request enough
+  // shared memory that no extra CTA is scheduled to spin in tcgen05.alloc
+  const int per_sm = 512 / a.tmem_cols;
+  size_t smem = tmem_smem_bytes(g, a.W);
+  const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
+  if (smem < cap) smem = cap;
+  int fpc = 1;
+  while (fpc < 8 && fpc * 2 <= n_frames &&
+         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 8LL * per_sm * sm_count())
+    fpc *= 2;
+  a.frames_per_cta = fpc;
+  const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
+  typedef void (*kfn)(const TmemArgs);
+  static const kfn table[16] = {
+      das_tmem_kernel<false, false, false, false>, das_tmem_kernel<false, false, false, true>,
+      das_tmem_kernel<false, false, true, false>,  das_tmem_kernel<false, false, true, true>,
+      das_tmem_kernel<false, true, false, false>,  das_tmem_kernel<false, true, false, true>,
+      das_tmem_kernel<false, true, true, false>,   das_tmem_kernel<false, true, true, true>,
+      das_tmem_kernel<true, false, false, false>,  das_tmem_kernel<true, false, false, true>,
+      das_tmem_kernel<true, false, true, false>,   das_tmem_kernel<true, false, true, true>,
+      das_tmem_kernel<true, true, false, false>,   das_tmem_kernel<true, true, false, true>,
+      das_tmem_kernel<true, true, true, false>,    das_tmem_kernel<true, true, true, true>};
+  const kfn k = table[(pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
+                      (g.rx_identity ? 1 : 0)];
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return BM_ERR_CUDA;
+  dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
+  k<<<grid, TTHREADS, smem, s>>>(a);
+  return cuda_status();
+}
+
+}  // namespace bm
