@@ -18,13 +18,13 @@
 // block (columns 8*(w&1).., rows 8*(w>>1)..), lane l the pixel pair
 // (row l/8, col l%8) / (row l/8 + 4, col l%8), so each gather of a warp is a
 // 4 x 8 pixel block (conflict-free, see das_fast_kernel).  RF windows are
-// staged per chunk of 64 channels with cp.async exactly as in
+// staged per chunk of 32 channels with cp.async exactly as in
 // das_fast_kernel.
 #include "bm_f32x2.cuh"
 
 namespace bm {
 
-constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 64;
+constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 32;
 
 struct TmemArgs {
   bm_das_geometry g;
@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
       M[j] = make_int2(len | (m << 13), (int)K);
     }
   };
-  // cp.async staging: 2 threads per channel, 16 B copies at fixed slots
-  // o = 4*(tid % 2) + 8*i, i < ceil(W / 8) <= 16
-  const int ld_jj = tid >> 1, ld_o = 4 * (tid & 1);
+  // cp.async staging: 4 threads per channel, 16 B copies at fixed slots
+  // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 8
+  const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
   const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
   auto issue_loads = [&](int q, const Cursor& cu) {
     const int j = cu.cb * TJC + ld_jj;
@@ -222,12 +222,12 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + cu.cb * TJC) * n_s + ld_trace;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int o = ld_o + 8 * i;
+    for (int i = 0; i < 8; ++i) {
+      const int o = ld_o + 16 * i;
       if (o < len) {
         const int s0 = ws + o;
         const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
-        cp_async16(wb + 32u * i, tr + (in ? ws + 8 * i : -ld_o), in ? 16 : 0);
+        cp_async16(wb + 64u * i, tr + (in ? ws + 16 * i : -ld_o), in ? 16 : 0);
       }
     }
   };
