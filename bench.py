@@ -40,7 +40,7 @@ WORKLOAD = "cfg2 PWI 128el x 11 angles x 2048 samples -> 512x512, DAS+envelope+d
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--frames", type=int, default=32, help="frames per GPU per step")
@@ -191,14 +191,15 @@ def main():
         return float(t.item())
 
     # ---- device-resident timed region --------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         eng.reconstruct(rf, out=out)
     torch.cuda.synchronize()
     eng.check()
     das_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.rows.clear()  # keep only samples taken from here on
     launches0 = eng.launches
     barrier()
     torch.cuda.synchronize()
@@ -260,25 +261,32 @@ def main():
     contrib = B * ctx.n_tx * ctx.n_elements * grid.n_z * grid.n_x
     sm_mhz = clk["sm_mhz"] or 1965.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # on-chip roofs: 8 FLOP and 8 B of gather per linear contribution
-    fp32_roof = n_sm * 256 * sm_mhz * 1e6            # FLOP/s
-    gather_roof = n_sm * 128 * sm_mhz * 1e6          # B/s (SMEM/L1 128 B/clk/SM)
-    t_fp32 = contrib * 8 / fp32_roof
-    t_gather = contrib * 8 / gather_roof
+    # Binding roof of DAS: the FP32 pipe.  The exact
+    # (bitwise) linear formulation is 9 FP32 lane-ops per contribution
+    # (t, floor, k0, a, 1-a, 2 rounded products, 2 adds; nearest: 4); the
+    # B200 FP32 pipe retires 128 lane-ops/clk/SM (profiles/r01_microbench.json:
+    # FADD2 = 2 warp-instr/clk/SM).  Shared-memory gathers (4 B each, 2 per
+    # contribution) run at 512 B/clk/SM (LDS.32 3.8 warp-instr/clk/SM), i.e.
+    # 64 contributions/clk/SM, far from binding; HBM is ~100x away.
+    ops = 9 if args.interp == "linear" else 4
+    t_fp32 = contrib * ops / (n_sm * 128 * sm_mhz * 1e6)
+    t_lds = contrib * 2 / (n_sm * 4 * 32 * sm_mhz * 1e6)
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-        "kernel": "bm_das_beamform (das_kernel)", "kernel_ms_per_launch": round(das_ms, 4),
+        "kernel": "bm_das_beamform (das_tmem_kernel)", "kernel_ms_per_launch": round(das_ms, 4),
         "algorithmic_bytes_per_launch": das_bytes,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-        "note": "DAS is not HBM-bound; its binding roof is on-chip (see binding)",
+        "note": "DAS is FP32-pipe bound, not HBM bound: see binding",
         "binding": {
-            "resource": "smem/L1 gather (8 B per linear contribution at 128 B/clk/SM)",
+            "resource": "FP32 pipe (9 lane-ops per linear contribution, 128 lane-ops/clk/SM)",
             "contributions_per_launch": contrib,
             "achieved_gcontrib_s": round(contrib / (das_ms / 1000.0) / 1e9, 1),
-            "t_gather_roof_ms": round(t_gather * 1000, 4),
+            "achieved_tflops_fp32_lane_ops": round(contrib * ops / (das_ms / 1000.0) / 1e12, 2),
+            "peak_tflops_fp32_lane_ops": round(n_sm * 128 * sm_mhz * 1e6 / 1e12, 2),
             "t_fp32_roof_ms": round(t_fp32 * 1000, 4),
-            "frac": round(max(t_gather, t_fp32) / (das_ms / 1000.0), 4),
+            "t_smem_gather_roof_ms": round(t_lds * 1000, 4),
+            "frac": round(t_fp32 / (das_ms / 1000.0), 4),
             "sm_mhz": sm_mhz, "n_sm": n_sm},
     }
 
