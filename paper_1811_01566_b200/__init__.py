@@ -8,7 +8,7 @@ Public names mirror echopipe/__init__.py:9-64 for the path.
 """
 
 from .beamform import INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform
-from . import engine
+from . import engine, parallel
 from .engine import BmodeEngine
 from .environment import (Environment, Phantom, SimulatorSource, default_pw_angles,
                           open_simulator, simulate_rf, wire_phantom)

@@ -1,0 +1,81 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU logic:
+frame partitioning and the lateral column split of one large frame with the
+all-reduce(MAX) of the peak and the gather of display slabs.  Per-rank
+compute is the CPU oracle here (test infrastructure); on GPUs it is the
+bm_* kernels (tests/test_gpu_parallel.py checks that path on one device)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1811_01566_b200 import parallel as P
+from paper_1811_01566_b200 import types as T
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_frame_partition_covers_all_frames():
+    for n in (0, 1, 7, 256):
+        for world in (1, 2, 3, 8):
+            got = [i for r in range(world) for i in P.frame_partition(n, world, r)]
+            assert got == list(range(n))
+            sizes = [len(P.frame_partition(n, world, r)) for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_column_slabs():
+    assert P.column_slabs(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert P.column_slabs(2048, 8)[7] == (1792, 2048)
+
+
+def _geometry():
+    ctx = T.AcquisitionContext(1540.0, 40e6, 16, 2e-4, T.StaScheme(tuple(range(16))))
+    ex = ctx.element_positions()
+    grid = T.ImageGrid(np.linspace(ex[0], ex[-1], 37), np.linspace(0, 512 * 1540 / 80e6, 64))
+    rf = np.random.default_rng(3).normal(size=(16, 16, 512)).astype(np.float32)
+    return ctx, grid, rf
+
+
+def _worker(rank, world, port, out_path):
+    from oracle import oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx, grid, rf = _geometry()
+        split = P.LateralSplit(grid, world, rank)
+        rf_slab = O.das_beamform(rf, ctx, split.sub_grid)                 # per-rank DAS
+        env = torch.from_numpy(np.abs(O.analytic_signal(rf_slab, axis=0)))  # rank-local lanes
+        rf_full = split.gather(torch.from_numpy(rf_slab))
+        disp = split.display(env, 30.0)
+        if rank == 0:
+            np.savez(out_path, rf=rf_full.numpy(), disp=disp.numpy())
+        else:
+            assert disp is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_lateral_split_gloo_matches_single_process(tmp_path, world):
+    from oracle import oracle as O
+
+    out = str(tmp_path / "out.npz")
+    mp.spawn(_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    got = np.load(out)
+    ctx, grid, rf = _geometry()
+    rf_ref, env_ref, disp_ref = O.bmode_chain(rf, ctx, grid)
+    # DAS is per pixel: the stitched slabs are bitwise the single-process image
+    assert got["rf"].tobytes() == rf_ref.tobytes()
+    # display against the all-reduced global peak
+    assert np.abs(got["disp"] - disp_ref).max() <= 1e-6
+    assert got["disp"].max() == 1.0
