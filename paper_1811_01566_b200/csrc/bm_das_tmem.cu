@@ -96,9 +96,53 @@ __device__ __forceinline__ void tm_ld32(uint32_t taddr, u64 (&d)[16]) {
   for (int i = 0; i < 16; ++i) d[i] = ((u64)r[2 * i + 1] << 32) | r[2 * i];
 }
 
-template <bool PW, bool LINEAR, bool T0, bool IDMAP>
-__global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a) {
+// Lane arithmetic: a thread owns PAIR ? two pixels (packed f32x2) : one pixel.
+template <bool PAIR> struct Lane;
+template <> struct Lane<true> {
+  typedef u64 T;
+  static __device__ __forceinline__ T splat(float a) { return pk(a, a); }
+  static __device__ __forceinline__ T make(float a, float b) { return pk(a, b); }
+  static __device__ __forceinline__ T add(T a, T b) { return add2(a, b); }
+  static __device__ __forceinline__ T add_rm(T a, T b) { return add2_rm(a, b); }
+  static __device__ __forceinline__ T sub(T a, T b) { return sub2(a, b); }
+  static __device__ __forceinline__ T mul(T a, T b) { return mul2(a, b); }
+};
+template <> struct Lane<false> {
+  typedef float T;
+  static __device__ __forceinline__ T splat(float a) { return a; }
+  static __device__ __forceinline__ T make(float a, float) { return a; }
+  static __device__ __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ T add_rm(T a, T b) { return __fadd_rd(a, b); }
+  static __device__ __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ T mul(T a, T b) { return __fmul_rn(a, b); }
+};
+
+__device__ __forceinline__ void tm_st1(uint32_t taddr, float a) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "f"(a) : "memory");
+}
+__device__ __forceinline__ float tm_ld1(uint32_t taddr) {
+  uint32_t a;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(a) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a)::"memory");
+  return __uint_as_float(a);
+}
+__device__ __forceinline__ void tm_ld32f(uint32_t taddr, float (&d)[32]) {
+  u64 p[16];
+  tm_ld32(taddr, p);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) unpk(p[i], d[2 * i], d[2 * i + 1]);
+}
+
+// PAIR: tile 16 x 16, thread = pixel pair (r, c) / (r + 4, c), TMEM columns 2m, 2m+1.
+// !PAIR: tile 8 x 16, thread = one pixel, TMEM column m, 4 CTAs per SM fit in TMEM.
+// Either way a warp's 32 gathers of one channel cover a 4 x 8 pixel block.
+template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP>
+__global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const TmemArgs a) {
   using O = R<float>;
+  using L = Lane<PAIR>;
+  typedef typename L::T VT;
+  constexpr int TZk = PAIR ? 16 : 8;
+  constexpr int CPE = PAIR ? 2 : 1;  // TMEM columns per element
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
   const int W = a.W;
@@ -117,9 +161,9 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int tiles_x = (g.n_x + TX - 1) / TX;
-  const int tz0 = (blockIdx.x / tiles_x) * TZ, tx0 = (blockIdx.x % tiles_x) * TX;
+  const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TX;
   const int col = tx0 + (warp & 1) * 8 + (lane & 7);
-  const int rowA = tz0 + (warp >> 1) * 8 + (lane >> 3), rowB = rowA + 4;
+  const int rowA = tz0 + (warp >> 1) * (PAIR ? 8 : 4) + (lane >> 3), rowB = rowA + 4;
   const int colc = min(col, g.n_x - 1);
   const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
 
@@ -141,17 +185,22 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
   const uint32_t tbase = *tmem_slot;
   const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
 
-  // ---- exact receive delays of the pixel pair -> TMEM columns 2m, 2m+1
+  // ---- exact receive delays of the thread's pixel(s) -> TMEM
   for (int m = 0; m < n_el; ++m) {
     const float dx = O::from_double(g.elem_x[m] - px);
     const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
-    const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
-    tm_st2(tlane + 2 * m, dA, dB);
+    if (PAIR) {
+      const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
+      tm_st2(tlane + 2 * m, dA, dB);
+    } else {
+      tm_st1(tlane + m, dA);
+    }
   }
   tm_wait_st();
 
+  const int zl = min(tz0 + TZk, g.n_z) - 1;
   const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TX, g.n_x) - 1];
-  const double z0 = g.z_pos[tz0], z1 = g.z_pos[min(tz0 + TZ, g.n_z) - 1];
+  const double z0 = g.z_pos[tz0], z1 = g.z_pos[zl];
   const double k = g.sampling_frequency / g.speed_of_sound;
   // receive-path delay bounds of element m over the tile rectangle (samples)
   // (float arithmetic: the window margins of 3-4 samples absorb its error)
@@ -239,12 +288,10 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
   cp_async_commit();
   nxt.next(n_chunks, n_tx);
 
-  const u64 M2 = pk(kMagic, kMagic);
-  const u64 NM2 = pk(-kMagic, -kMagic);
-  const u64 ONE2 = pk(1.0f, 1.0f);
-  const u64 HALF2 = pk(0.5f, 0.5f);
-  u64 acc = 0ull;  // (+0.0f, +0.0f)
-  u64 txd = 0ull, t0e2 = 0ull;
+  const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
+  const VT ONE2 = L::splat(1.0f), HALF2 = L::splat(0.5f);
+  VT acc = L::splat(0.0f);  // +0.0f
+  VT txd = acc, t0e2 = acc;
 
   for (int q = 0; q < Q; ++q) {
     __syncthreads();  // compute(q-1) done everywhere: buffer (q+1)&1 may be refilled
@@ -261,13 +308,14 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
         const float sa = reinterpret_cast<const float*>(g.sin_a)[cur.e];
         const float xs = O::mul(pxd, sa);
         const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
-        const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
-        txd = pk(tA, tB);
+        const float tB = PAIR ? O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c)) : tA;
+        txd = L::make(tA, tB);
+      } else if (PAIR) {
+        txd = (VT)tm_ld2(tlane + 2 * g.tx_elements[cur.e]);
       } else {
-        txd = tm_ld2(tlane + 2 * g.tx_elements[cur.e]);
+        txd = L::make(tm_ld1(tlane + g.tx_elements[cur.e]), 0.0f);
       }
-      const float t0 = t0s[cur.e];
-      t0e2 = pk(t0, t0);
+      t0e2 = L::splat(t0s[cur.e]);
     }
     cp_async_wait1();
     __syncthreads();  // chunk q staged and visible
@@ -275,56 +323,71 @@ __global__ void __launch_bounds__(TTHREADS, 2) das_tmem_kernel(const TmemArgs a)
     const int2* M = meta + (cur.T & 1) * n_rx + cur.cb * TJC;
     const int jn = min(TJC, n_rx - cur.cb * TJC);
 
-    // one channel: rxd = receive delays of the pair, mm = staging metadata
-    auto channel = [&](u64 rxd, int2 mm) {
-      u64 t = add2(txd, rxd);
-      if (T0) t = sub2(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
-      const uint32_t K = (uint32_t)mm.y;
-      if (LINEAR) {
-        const u64 r = add2_rm(t, M2);   // floor(t) + 1.5*2^23, exactly
-        float rA, rB;
-        unpk(r, rA, rB);
-        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
-        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
-        const u64 x0 = pk(lds0(aA), lds0(aB));
-        const u64 x1 = pk(lds1(aA), lds1(aB));
-        const u64 fr = sub2(t, add2(r, NM2));  // a = t - floor(t)
-        const u64 om = sub2(ONE2, fr);         // 1 - a
-        acc = add2(acc, mul2(om, x0));         // acc = out + (1 - a) * x[k0]
-        acc = add2(acc, mul2(fr, x1));         // out = acc + a * x[k1]
+    // one channel: rxd = receive delay(s), K = gather address base
+    auto channel = [&](VT rxd, uint32_t K) {
+      VT t = L::add(txd, rxd);
+      if (T0) t = L::sub(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
+      const VT r = LINEAR ? L::add_rm(t, M2) : L::add_rm(L::add(t, HALF2), M2);
+      float rA, rB;
+      if (PAIR) {
+        unpk((u64)r, rA, rB);
       } else {
-        const u64 r = add2_rm(add2(t, HALF2), M2);  // floor(t + 0.5)
-        float rA, rB;
-        unpk(r, rA, rB);
-        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
-        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
-        acc = add2(acc, pk(lds0(aA), lds0(aB)));
+        rA = (float)r;
+        rB = rA;
+      }
+      const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+      const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
+      if (LINEAR) {
+        const VT x0 = L::make(lds0(aA), PAIR ? lds0(aB) : 0.0f);
+        const VT x1 = L::make(lds1(aA), PAIR ? lds1(aB) : 0.0f);
+        const VT fr = L::sub(t, L::add(r, NM2));  // a = t - floor(t)
+        const VT om = L::sub(ONE2, fr);           // 1 - a
+        acc = L::add(acc, L::mul(om, x0));        // acc = out + (1 - a) * x[k0]
+        acc = L::add(acc, L::mul(fr, x1));        // out = acc + a * x[k1]
+      } else {
+        acc = L::add(acc, L::make(lds0(aA), PAIR ? lds0(aB) : 0.0f));
       }
     };
     if (IDMAP && jn == TJC) {
       // identity map: channels cb*32 .. cb*32+31 are elements of the same
-      // index -- two tcgen05.ld.x32 fetch all 32 delay pairs
+      // index -- tcgen05.ld.x32 fetches 16 delay pairs (PAIR) or 32 delays
+      if (PAIR) {
 #pragma unroll
-      for (int h = 0; h < TJC; h += 16) {
-        u64 d[16];
-        tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
+        for (int h = 0; h < TJC; h += 16) {
+          u64 d[16];
+          tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) channel(d[i], M[h + i]);
+          for (int i = 0; i < 16; ++i) channel((VT)d[i], (uint32_t)M[h + i].y);
+        }
+      } else {
+        float d[32];
+        tm_ld32f(tlane + cur.cb * TJC, d);
+#pragma unroll
+        for (int i = 0; i < TJC; ++i) channel(L::make(d[i], 0.0f), (uint32_t)M[i].y);
       }
     } else {
       for (int jj = 0; jj < jn; ++jj) {
         const int2 mm = M[jj];
-        channel(tm_ld2(tlane + 2 * ((unsigned)mm.x >> 13)), mm);
+        const uint32_t col_m = CPE * ((unsigned)mm.x >> 13);
+        const VT rxd = PAIR ? (VT)tm_ld2(tlane + col_m) : L::make(tm_ld1(tlane + col_m), 0.0f);
+        channel(rxd, (uint32_t)mm.y);
       }
     }
 
     if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
       const int64_t fo = (int64_t)(f_begin + cur.fl) * a.out_stride;
       if (col < g.n_x) {
-        if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = lo_f(acc);
-        if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = hi_f(acc);
+        float oA, oB;
+        if (PAIR) {
+          unpk((u64)acc, oA, oB);
+        } else {
+          oA = (float)acc;
+          oB = 0.0f;
+        }
+        if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
+        if (PAIR && rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = oB;
       }
-      acc = 0ull;
+      acc = L::splat(0.0f);
     }
     cur.next(n_chunks, n_tx);
   }
@@ -344,9 +407,9 @@ static size_t tmem_smem_bytes(const bm_das_geometry& g, int W) {
   return b + (size_t)2 * TJC * W * 4;
 }
 
-static int tmem_cols_for(int n_el) {
+static int tmem_cols_for(int n_el, bool pair) {
   int cols = 32;
-  while (cols < 2 * n_el) cols *= 2;
+  while (cols < (pair ? 2 : 1) * n_el) cols *= 2;
   return cols;
 }
 
@@ -354,19 +417,30 @@ int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (g.window_hint > 128) return 0;              // loader: <= 8 copies of 16 B per thread
-  if (2 * g.n_elements > 512) return 0;          // one TMEM column pair per element
+  if (g.n_elements > 512) return 0;              // one TMEM column per element (scalar)
   if (tmem_smem_bytes(g, g.window_hint) > 110 * 1024) return 0;
   return 1;
 }
 
+// BM_DAS_LANES = pair (default) | scalar: pixels per thread in the TMEM kernel
+static bool tmem_pair_choice(const bm_das_geometry& g) {
+  const char* e = getenv("BM_DAS_LANES");
+  if (e && !strcmp(e, "scalar")) return false;
+  if (e && !strcmp(e, "pair")) return 2 * g.n_elements <= 512;
+  return 2 * g.n_elements <= 512;
+}
+
 int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                     int64_t out_stride, int n_frames, cudaStream_t s) {
+  const bool pair = tmem_pair_choice(g);
   TmemArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1,
-             g.window_hint, tmem_cols_for(g.n_elements)};
-  const int tiles = ((g.n_z + TZ - 1) / TZ) * ((g.n_x + TX - 1) / TX);
+             g.window_hint, tmem_cols_for(g.n_elements, pair)};
+  const int tz = pair ? 16 : 8;
+  const int tiles = ((g.n_z + tz - 1) / tz) * ((g.n_x + TX - 1) / TX);
   // CTAs per SM are limited to what TMEM holds (512 columns): request enough
   // shared memory that no extra CTA is scheduled to spin in tcgen05.alloc
-  const int per_sm = 512 / a.tmem_cols;
+  int per_sm = 512 / a.tmem_cols;
+  if (per_sm > 4) per_sm = 4;
   size_t smem = tmem_smem_bytes(g, a.W);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   if (smem < cap) smem = cap;
@@ -377,16 +451,18 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   a.frames_per_cta = fpc;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const TmemArgs);
-  static const kfn table[16] = {
-      das_tmem_kernel<false, false, false, false>, das_tmem_kernel<false, false, false, true>,
-      das_tmem_kernel<false, false, true, false>,  das_tmem_kernel<false, false, true, true>,
-      das_tmem_kernel<false, true, false, false>,  das_tmem_kernel<false, true, false, true>,
-      das_tmem_kernel<false, true, true, false>,   das_tmem_kernel<false, true, true, true>,
-      das_tmem_kernel<true, false, false, false>,  das_tmem_kernel<true, false, false, true>,
-      das_tmem_kernel<true, false, true, false>,   das_tmem_kernel<true, false, true, true>,
-      das_tmem_kernel<true, true, false, false>,   das_tmem_kernel<true, true, false, true>,
-      das_tmem_kernel<true, true, true, false>,    das_tmem_kernel<true, true, true, true>};
-  const kfn k = table[(pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
+#define BM_TMEM_ROW(P)                                                                       \
+  das_tmem_kernel<P, false, false, false, false>, das_tmem_kernel<P, false, false, false, true>, \
+      das_tmem_kernel<P, false, false, true, false>, das_tmem_kernel<P, false, false, true, true>, \
+      das_tmem_kernel<P, false, true, false, false>, das_tmem_kernel<P, false, true, false, true>, \
+      das_tmem_kernel<P, false, true, true, false>, das_tmem_kernel<P, false, true, true, true>,   \
+      das_tmem_kernel<P, true, false, false, false>, das_tmem_kernel<P, true, false, false, true>, \
+      das_tmem_kernel<P, true, false, true, false>, das_tmem_kernel<P, true, false, true, true>,   \
+      das_tmem_kernel<P, true, true, false, false>, das_tmem_kernel<P, true, true, false, true>,   \
+      das_tmem_kernel<P, true, true, true, false>, das_tmem_kernel<P, true, true, true, true>
+  static const kfn table[32] = {BM_TMEM_ROW(false), BM_TMEM_ROW(true)};
+#undef BM_TMEM_ROW
+  const kfn k = table[(pair ? 16 : 0) | (pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
                       (g.rx_identity ? 1 : 0)];
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return BM_ERR_CUDA;

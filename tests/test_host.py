@@ -138,13 +138,17 @@ def test_no_contracted_fma_in_das_kernels():
     the correctly-rounded sqrt/div sequences."""
     funcs = _sass_by_function()
     das = {n: l for n, l in funcs.items() if "das_fast_kernel" in n or "das_tmem_kernel" in n}
-    # 2 kernels x {STA, PW} x {nearest, linear} x {t0, no t0} x {identity map, general}
-    assert len(das) == 32
+    # (smem, tmem-pair, tmem-scalar) x {STA, PW} x {nearest, linear} x {t0, no t0}
+    # x {identity map, general}
+    assert len(das) == 48
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
                 assert "RZ" in l.split("FFMA2", 1)[1].split(";")[0], (n, l)
-        assert any("FADD2.RM" in l for l in lines), n  # packed floor, magic constant
+        # floor via the magic constant, rounding toward -inf: packed (FADD2) for
+        # the pair kernels, scalar for the one-pixel-per-thread TMEM kernel
+        packed = not n.startswith("_ZN2bm15das_tmem_kernelILb0")
+        assert any(("FADD2.RM" if packed else "FADD.RM") in l for l in lines), n
         assert any("LDGSTS" in l for l in lines), n    # cp.async staging
         if "das_tmem_kernel" in n:  # receive-delay table in tensor memory
             assert any("LDTM" in l for l in lines) and any("STTM" in l for l in lines), n
