@@ -24,7 +24,7 @@
 
 namespace bm {
 
-constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 32;
+constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 32, NST = 3;
 
 struct TmemArgs {
   bm_das_geometry g;
@@ -151,12 +151,12 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int off_tmin = 16;
   const int off_meta = (off_tmin + 8 * n_tx + 15) & ~15;
-  const int off_win = (off_meta + 16 * n_rx + 15) & ~15;
+  const int off_win = (off_meta + 24 * n_rx + 15) & ~15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
   float* tmin = reinterpret_cast<float*>(smem_raw + off_tmin);  // [n_tx]
   float* tmax = tmin + n_tx;                                    // [n_tx]
-  int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [2][n_rx]
-  float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [2][TJC][W]
+  int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [3][n_rx]
+  float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [NST][TJC][W]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   //   x = staged length | element m << 13,  y = K (gather address base)
   auto make_meta = [&](int T) {
     const int e = T % n_tx;
-    int2* M = meta + (T & 1) * n_rx;
+    int2* M = meta + (T % 3) * n_rx;
     const float t0 = t0s[e];
     const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
     const int* map = g.rx_map + (int64_t)e * n_rx;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       const int hi = (int)floorf(hi_e + rhi) + 4;
       const int len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
       const int cb = j / TJC, jj = j - cb * TJC;
-      const int buf = (T * n_chunks + cb) & 1;
+      const int buf = (T * n_chunks + cb) % NST;
       const uint32_t K = win_s + (uint32_t)((buf * TJC + jj) * W) * 4u -
                          (uint32_t)(kMagicBits + ws) * 4u;
       M[j] = make_int2(len | (m << 13), (int)K);
@@ -262,31 +262,55 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   auto issue_loads = [&](int q, const Cursor& cu) {
     const int j = cu.cb * TJC + ld_jj;
     if (j >= n_rx) return;
-    const int2 mm = meta[(cu.T & 1) * n_rx + j];
+    const int2 mm = meta[(cu.T % 3) * n_rx + j];
     const int len = mm.x & 0x1fff;
-    const uint32_t wb = win_s + (uint32_t)(((q & 1) * TJC + ld_jj) * W + ld_o) * 4u;
+    const uint32_t wb = win_s + (uint32_t)(((q % NST) * TJC + ld_jj) * W + ld_o) * 4u;
     // K = wb0 - 4*(M_bits + ws) mod 2^32, so (wb0 - K)/4 = (M_bits + ws) mod 2^30
     const int ws = (int)((wb - (uint32_t)ld_o * 4u - (uint32_t)mm.y) >> 2) -
                    (kMagicBits & 0x3fffffff);
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + cu.cb * TJC) * n_s + ld_trace;
+    // all 8 copies from distinct address registers (no write-after-read
+    // stall on a register an in-flight cp.async still reads)
+    const float* src[8];
+    int nb[8], act[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int o = ld_o + 16 * i;
-      if (o < len) {
-        const int s0 = ws + o;
-        const bool in = (unsigned)s0 <= (unsigned)(n_s - 4);
-        cp_async16(wb + 64u * i, tr + (in ? ws + 16 * i : -ld_o), in ? 16 : 0);
-      }
+      const bool in = (unsigned)(ws + o) <= (unsigned)(n_s - 4);
+      src[i] = tr + (in ? ws + 16 * i : -ld_o);
+      nb[i] = in ? 16 : 0;
+      act[i] = o < len;
     }
+#pragma unroll
+    for (int h = 0; h < 8; h += 4)
+      asm volatile(
+          "{\n .reg .pred q0, q1, q2, q3;\n"
+          " setp.ne.b32 q0, %12, 0;\n setp.ne.b32 q1, %13, 0;\n"
+          " setp.ne.b32 q2, %14, 0;\n setp.ne.b32 q3, %15, 0;\n"
+          " @q0 cp.async.cg.shared.global [%0], [%4], 16, %8;\n"
+          " @q1 cp.async.cg.shared.global [%1], [%5], 16, %9;\n"
+          " @q2 cp.async.cg.shared.global [%2], [%6], 16, %10;\n"
+          " @q3 cp.async.cg.shared.global [%3], [%7], 16, %11;\n}\n" ::"r"(wb + 64u * h),
+          "r"(wb + 64u * (h + 1)), "r"(wb + 64u * (h + 2)), "r"(wb + 64u * (h + 3)),
+          "l"(src[h]), "l"(src[h + 1]), "l"(src[h + 2]), "l"(src[h + 3]), "r"(nb[h]),
+          "r"(nb[h + 1]), "r"(nb[h + 2]), "r"(nb[h + 3]), "r"(act[h]), "r"(act[h + 1]),
+          "r"(act[h + 2]), "r"(act[h + 3])
+          : "memory");
   };
 
-  Cursor cur{0, 0, 0, 0}, nxt{0, 0, 0, 0};
+  // 3-stage cp.async pipeline, one barrier per chunk: at iteration q the
+  // barrier both publishes chunk q and retires chunk q-1, whose buffer
+  // ((q+2) % 3) is then refilled with chunk q+2.
+  Cursor cur{0, 0, 0, 0}, nx2{0, 0, 0, 0};
   make_meta(0);
+  if (n_T > 1) make_meta(1);
   __syncthreads();
-  issue_loads(0, nxt);
-  cp_async_commit();
-  nxt.next(n_chunks, n_tx);
+  for (int p = 0; p < 2; ++p) {
+    if (p < Q) issue_loads(p, nx2);
+    cp_async_commit();
+    nx2.next(n_chunks, n_tx);
+  }
 
   const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
   const VT ONE2 = L::splat(1.0f), HALF2 = L::splat(0.5f);
@@ -294,14 +318,15 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   VT txd = acc, t0e2 = acc;
 
   for (int q = 0; q < Q; ++q) {
-    __syncthreads();  // compute(q-1) done everywhere: buffer (q+1)&1 may be refilled
-    if (cur.cb == 0 && cur.T + 1 < n_T) {
-      make_meta(cur.T + 1);  // ring slot of transmit T-1: all its loads/computes are done
-      __syncthreads();
+    cp_async_wait1();  // this thread's copies of chunk q have landed
+    __syncthreads();   // chunk q visible; compute(q-1) retired everywhere
+    if (cur.cb == 0 && cur.T + 2 < n_T) {
+      make_meta(cur.T + 2);  // ring slot of transmit T-1: retired
+      if (n_chunks < 2) __syncthreads();  // first used by this iteration's loads
     }
-    if (q + 1 < Q) issue_loads(q + 1, nxt);
+    if (q + 2 < Q) issue_loads(q + 2, nx2);
     cp_async_commit();
-    nxt.next(n_chunks, n_tx);
+    nx2.next(n_chunks, n_tx);
     if (cur.cb == 0) {
       if (PW) {
         const float ca = reinterpret_cast<const float*>(g.cos_a)[cur.e];
@@ -317,10 +342,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       }
       t0e2 = L::splat(t0s[cur.e]);
     }
-    cp_async_wait1();
-    __syncthreads();  // chunk q staged and visible
-
-    const int2* M = meta + (cur.T & 1) * n_rx + cur.cb * TJC;
+    const int2* M = meta + (cur.T % 3) * n_rx + cur.cb * TJC;
     const int jn = min(TJC, n_rx - cur.cb * TJC);
 
     // one channel: rxd = receive delay(s), K = gather address base
@@ -402,9 +424,9 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
 
 static size_t tmem_smem_bytes(const bm_das_geometry& g, int W) {
   size_t b = 16 + (size_t)g.n_tx * 8;
-  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 16;
+  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 24;
   b = (b + 15) & ~size_t(15);
-  return b + (size_t)2 * TJC * W * 4;
+  return b + (size_t)NST * TJC * W * 4;
 }
 
 static int tmem_cols_for(int n_el, bool pair) {
