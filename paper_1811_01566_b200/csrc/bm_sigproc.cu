@@ -61,47 +61,55 @@ __device__ __forceinline__ void block_peak(T v, typename PeakBits<T>::U* peak) {
 
 enum OutMode { kComplex = 0, kEnvelope = 1 };
 
-// Power-of-two lanes: L lanes of length n per CTA, radix-2 DIT in shared memory.
+// Power-of-two lanes: L (a power of two) lanes of length n per CTA, radix-2
+// DIT in shared memory.  All index arithmetic is 32-bit shifts and masks
+// (n, L powers of two); consecutive threads touch consecutive lanes on
+// global loads/stores (coalesced rows of L values) and consecutive
+// butterflies of one lane in shared memory.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict__ x, T* __restrict__ out,
                                                             typename PeakBits<T>::U* __restrict__ peak,
-                                                            int64_t n, int log2n, int64_t inner,
-                                                            int L) {
+                                                            int n, int log2n, int64_t inner,
+                                                            int log2L) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = 1 << log2L;
   V* tw = reinterpret_cast<V*>(smem_raw);  // [n/2]
   V* buf = tw + n / 2;                       // [L][n]
   const int64_t o = blockIdx.y;
   const int64_t i_base = (int64_t)blockIdx.x * L;
-  const int lanes = (int)((inner - i_base) < L ? (inner - i_base) : L);
-  const int64_t half_n = n >> 1;
+  const int half_n = n >> 1;
+  const int nt = blockDim.x;
 
-  for (int64_t k = threadIdx.x; k < half_n; k += blockDim.x) {
+  for (int k = threadIdx.x; k < half_n; k += nt) {
     double s, c;
     sincospi(-2.0 * (double)k / (double)n, &s, &c);
     tw[k] = V{(T)c, (T)s};
   }
-  const T* xo = x + o * n * inner + i_base;
-  for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
-    const int64_t k = idx / lanes;
-    const int l = (int)(idx % lanes);
-    const int64_t r = __brevll((unsigned long long)k) >> (64 - log2n);
-    buf[l * n + r] = V{xo[k * inner + l], T(0)};
+  const T* xo = x + o * (int64_t)n * inner + i_base;
+  const bool full = i_base + L <= inner;
+  for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
+    const int l = idx & (L - 1), k = idx >> log2L;
+    const int r = __brev(k) >> (32 - log2n);
+    T v = T(0);
+    if (full || i_base + l < inner) v = xo[(int64_t)k * inner + l];
+    buf[(l << log2n) + r] = V{v, T(0)};
   }
   __syncthreads();
 
+  const int nb = half_n << log2L;  // butterflies per pass
   for (int pass = 0; pass < 2; ++pass) {
     const T sign = pass == 0 ? T(1) : T(-1);  // inverse: conjugate twiddles
     for (int s = 1; s <= log2n; ++s) {
-      const int64_t h = (int64_t)1 << (s - 1);
-      for (int64_t b = threadIdx.x; b < half_n * lanes; b += blockDim.x) {
-        const int l = (int)(b / half_n);
-        const int64_t bb = b % half_n;
-        const int64_t pos = bb & (h - 1);
-        const int64_t i = ((bb >> (s - 1)) << s) + pos;
+      const int h = 1 << (s - 1);
+      for (int b = threadIdx.x; b < nb; b += nt) {
+        const int l = b >> (log2n - 1);
+        const int bb = b & (half_n - 1);
+        const int pos = bb & (h - 1);
+        const int i = ((bb >> (s - 1)) << s) + pos;
         V w = tw[pos << (log2n - s)];
         w.y *= sign;
-        V* lane = buf + l * n;
+        V* lane = buf + (l << log2n);
         const V u = lane[i];
         const V t = cmul<T>(w, lane[i + h]);
         lane[i] = V{u.x + t.x, u.y + t.y};
@@ -111,12 +119,11 @@ __global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict_
     }
     if (pass == 0) {
       // one-sided gain, then bit-reverse permutation for the inverse DIT
-      for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
-        const int l = (int)(idx / n);
-        const int64_t k = idx % n;
-        const int64_t r = __brevll((unsigned long long)k) >> (64 - log2n);
+      for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
+        const int l = idx >> log2n, k = idx & (n - 1);
+        const int r = __brev(k) >> (32 - log2n);
         if (k > r) continue;
-        V* lane = buf + l * n;
+        V* lane = buf + (l << log2n);
         const T gk = hilbert_gain<T>(k, n), gr = hilbert_gain<T>(r, n);
         const V a = lane[k], bv = lane[r];
         lane[k] = V{bv.x * gr, bv.y * gr};
@@ -128,12 +135,12 @@ __global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict_
 
   const T inv_n = T(1) / T(n);
   T vmax = T(0);
-  for (int64_t idx = threadIdx.x; idx < n * lanes; idx += blockDim.x) {
-    const int64_t k = idx / lanes;
-    const int l = (int)(idx % lanes);
-    const V z = buf[l * n + k];
+  for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
+    const int l = idx & (L - 1), k = idx >> log2L;
+    if (!full && i_base + l >= inner) continue;
+    const V z = buf[(l << log2n) + k];
     const T re = z.x * inv_n, im = z.y * inv_n;
-    const int64_t g = o * n * inner + k * inner + i_base + l;
+    const int64_t g = o * (int64_t)n * inner + (int64_t)k * inner + i_base + l;
     if (MODE == kComplex) {
       reinterpret_cast<V*>(out)[g] = V{re, im};
     } else {
@@ -281,18 +288,23 @@ static int launch_analytic(const T* x, T* out, typename PeakBits<T>::U* peak, in
   using V = typename C2<T>::type;
   if (outer > 65535) return BM_ERR_UNSUPPORTED;
   if (is_pow2(n)) {
+    if (n > (1 << 20) || inner > (int64_t)1 << 40) return BM_ERR_UNSUPPORTED;
     const size_t lane_bytes = (size_t)n * sizeof(V);
     const size_t tw_bytes = (size_t)(n / 2) * sizeof(V);
-    int L = (int)((96 * 1024) / lane_bytes);
-    L = L < 1 ? 1 : (L > 16 ? 16 : L);
-    if (L > inner) L = (int)inner;
-    const size_t smem = tw_bytes + L * lane_bytes;
+    // lanes per CTA: a power of two, enough for 32 B row segments when the
+    // image is wide, few enough to give >= 2 waves of CTAs
+    int log2L = 0;
+    while ((2 << log2L) <= 8 && (2 << log2L) <= inner &&
+           tw_bytes + (size_t)(2 << log2L) * lane_bytes <= 96 * 1024)
+      ++log2L;
+    const size_t smem = tw_bytes + ((size_t)1 << log2L) * lane_bytes;
     if (smem > 220 * 1024) return BM_ERR_UNSUPPORTED;
     auto k = analytic_pow2_kernel<T, MODE>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return BM_ERR_CUDA;
+    const int64_t L = (int64_t)1 << log2L;
     dim3 grid((unsigned)((inner + L - 1) / L), (unsigned)outer);
-    k<<<grid, 256, smem, s>>>(x, out, peak, n, ilog2(n), inner, L);
+    k<<<grid, 256, smem, s>>>(x, out, peak, (int)n, ilog2(n), inner, log2L);
   } else {
     const size_t smem = (size_t)n * sizeof(V) + (size_t)(n / 2 + 1) * sizeof(V) + (size_t)n * sizeof(T);
     if (smem > 220 * 1024 || inner > 0x7fffffff) return BM_ERR_UNSUPPORTED;
