@@ -122,49 +122,68 @@ class BmodeEngine:
         current stream.  Returns ``disp_host`` after synchronising."""
         import torch
 
-        f = int(rf_host.shape[0])
         if disp_host is None:
-            disp_host = torch.empty((f,) + self.image_shape, dtype=self.tdtype,
-                                    pin_memory=True)
-        chunk = max(1, min(chunk, f))
-        n_s = int(rf_host.shape[-1])
+            disp_host = torch.empty((int(rf_host.shape[0]),) + self.image_shape,
+                                    dtype=self.tdtype, pin_memory=True)
+        self.reconstruct_host_stream([(rf_host, disp_host)], chunk=chunk)
+        return disp_host
+
+    def reconstruct_host_stream(self, batches, chunk: int = 2):
+        """A stream of host batches ``[(rf_host, disp_host), ...]`` reconstructed
+        as one continuous chunk pipeline (H2D of chunk i+1 and D2H of chunk
+        i-1 overlap the reconstruction of chunk i, across batch boundaries),
+        synchronising once at the end.  Every batch's RF is copied in and its
+        display copied out."""
+        import torch
+
+        batches = list(batches)
+        if not batches:
+            return
+        n_s = int(batches[0][0].shape[-1])
+        chunk = max(1, chunk)
+        nbuf = 3
         key = ("host", chunk, n_s)
         if key not in self._ws:
             bufs = [torch.empty((chunk,) + self.frame_shape + (n_s,), dtype=self.tdtype,
-                                device=self.device) for _ in range(2)]
+                                device=self.device) for _ in range(nbuf)]
             outs = [torch.empty((chunk,) + self.image_shape, dtype=self.tdtype,
-                                device=self.device) for _ in range(2)]
+                                device=self.device) for _ in range(nbuf)]
             self._ws[key] = (bufs, outs, torch.cuda.Stream(self.device),
                              torch.cuda.Stream(self.device))
         bufs, outs, h2d, d2h = self._ws[key]
         comp = torch.cuda.current_stream(self.device)
-        n_chunks = (f + chunk - 1) // chunk
-        up_done = [None, None]
-        comp_done = [None, None]
-        down_done = [None, None]
-        status = torch.zeros(f, dtype=torch.int32, device=self.device)
+        up_done = [None] * nbuf
+        comp_done = [None] * nbuf
+        down_done = [None] * nbuf
+        total = sum(int(rf.shape[0]) for rf, _ in batches)
+        status = torch.zeros(total, dtype=torch.int32, device=self.device)
         self._last_status = status
-        for i in range(n_chunks):
-            slot = i % 2
-            lo, hi = i * chunk, min(f, (i + 1) * chunk)
-            with torch.cuda.stream(h2d):
-                if comp_done[slot] is not None:
-                    h2d.wait_event(comp_done[slot])  # slot's rf buffer free again
-                bufs[slot][: hi - lo].copy_(rf_host[lo:hi], non_blocking=True)
-                up_done[slot] = torch.cuda.Event()
-                up_done[slot].record(h2d)
-            comp.wait_event(up_done[slot])
-            if down_done[slot] is not None:
-                comp.wait_event(down_done[slot])  # slot's output buffer drained
-            self.reconstruct(bufs[slot][: hi - lo], out=outs[slot][: hi - lo], stream=comp,
-                             key=("host", chunk), status=status[lo:hi])
-            comp_done[slot] = torch.cuda.Event()
-            comp_done[slot].record(comp)
-            with torch.cuda.stream(d2h):
-                d2h.wait_event(comp_done[slot])
-                disp_host[lo:hi].copy_(outs[slot][: hi - lo], non_blocking=True)
-                down_done[slot] = torch.cuda.Event()
-                down_done[slot].record(d2h)
+        i = 0
+        base = 0
+        for rf_host, disp_host in batches:
+            f = int(rf_host.shape[0])
+            for lo in range(0, f, chunk):
+                hi = min(f, lo + chunk)
+                slot = i % nbuf
+                with torch.cuda.stream(h2d):
+                    if comp_done[slot] is not None:
+                        h2d.wait_event(comp_done[slot])  # slot's rf buffer free again
+                    bufs[slot][: hi - lo].copy_(rf_host[lo:hi], non_blocking=True)
+                    up_done[slot] = torch.cuda.Event()
+                    up_done[slot].record(h2d)
+                comp.wait_event(up_done[slot])
+                if down_done[slot] is not None:
+                    comp.wait_event(down_done[slot])  # slot's output buffer drained
+                self.reconstruct(bufs[slot][: hi - lo], out=outs[slot][: hi - lo], stream=comp,
+                                 key=("host", chunk), status=status[base + lo:base + hi])
+                comp_done[slot] = torch.cuda.Event()
+                comp_done[slot].record(comp)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(comp_done[slot])
+                    disp_host[lo:hi].copy_(outs[slot][: hi - lo], non_blocking=True)
+                    down_done[slot] = torch.cuda.Event()
+                    down_done[slot].record(d2h)
+                i += 1
+            base += f
         d2h.synchronize()
         comp.synchronize()
-        return disp_host
