@@ -466,9 +466,11 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   size_t smem = tmem_smem_bytes(g, a.W);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   if (smem < cap) smem = cap;
+  // frames per CTA: amortise the per-CTA delay-table build over a frame
+  // group while keeping >= 4 waves of CTAs for load balance
   int fpc = 1;
-  while (fpc < 8 && fpc * 2 <= n_frames &&
-         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 8LL * per_sm * sm_count())
+  while (fpc < 16 && fpc * 2 <= n_frames &&
+         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
     fpc *= 2;
   a.frames_per_cta = fpc;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;

@@ -128,7 +128,7 @@ class BmodeEngine:
         self.reconstruct_host_stream([(rf_host, disp_host)], chunk=chunk)
         return disp_host
 
-    def reconstruct_host_stream(self, batches, chunk: int = 2):
+    def reconstruct_host_stream(self, batches, chunk: int = 8):
         """A stream of host batches ``[(rf_host, disp_host), ...]`` reconstructed
         as one continuous chunk pipeline (H2D of chunk i+1 and D2H of chunk
         i-1 overlap the reconstruction of chunk i, across batch boundaries),
