@@ -24,7 +24,7 @@
 
 namespace bm {
 
-constexpr int TZ = 16, TX = 16, TTHREADS = 128, TJC = 32, NST = 3;
+constexpr int TX = 16, TTHREADS = 128, TJC = 32, NST = 3;
 
 struct TmemArgs {
   bm_das_geometry g;
@@ -149,13 +149,21 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
 
   // shared memory: [tmem base][tmin|tmax][meta ring][windows]
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // [tmem base][tmin|tmax|t0|tx sel][rmin|rmax][meta ring][PW tx delays][windows]
   const int off_tmin = 16;
-  const int off_meta = (off_tmin + 8 * n_tx + 15) & ~15;
-  const int off_win = (off_meta + 24 * n_rx + 15) & ~15;
+  const int off_rmin = (off_tmin + 16 * n_tx + 15) & ~15;
+  const int off_meta = (off_rmin + 8 * n_el + 15) & ~15;
+  const int off_txd = (off_meta + 24 * n_rx + 15) & ~15;
+  const int off_win = off_txd + (PW ? n_tx * TTHREADS * (int)sizeof(u64) : 0);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
   float* tmin = reinterpret_cast<float*>(smem_raw + off_tmin);  // [n_tx]
   float* tmax = tmin + n_tx;                                    // [n_tx]
+  float* t0v = tmax + n_tx;                                     // [n_tx] fs*t0
+  int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
+  float* rmin = reinterpret_cast<float*>(smem_raw + off_rmin);  // [n_el]
+  float* rmax = rmin + n_el;                                    // [n_el]
   int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [3][n_rx]
+  u64* txd_s = reinterpret_cast<u64*>(smem_raw + off_txd);      // PW: [n_tx][128]
   float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [NST][TJC][W]
 
   const int tid = threadIdx.x;
@@ -212,7 +220,10 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     lo = kf * sqrtf(dmin * dmin + z0f * z0f);
     hi = kf * sqrtf(dmax * dmax + z1f * z1f);
   };
+  for (int m = tid; m < n_el; m += TTHREADS) rx_bounds(m, rmin[m], rmax[m]);
   for (int e = tid; e < n_tx; e += TTHREADS) {
+    t0v[e] = reinterpret_cast<const float*>(g.t0_smp)[e];
+    if (!PW) txe[e] = g.tx_elements[e];
     if (PW) {
       const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
       const double sa = reinterpret_cast<const float*>(g.sin_a)[e];
@@ -224,9 +235,21 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
     }
   }
+  if (PW) {
+    // exact transmit delays fs*((z cos + x sin)/c) of the thread's pixels for
+    // every angle, once per CTA (beamform.py:218-225)
+    for (int e = 0; e < n_tx; ++e) {
+      const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
+      const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+      const float xs = O::mul(pxd, sa);
+      const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+      const float tB = PAIR ? O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c)) : tA;
+      txd_s[e * TTHREADS + tid] = pk(tA, tB);
+    }
+  }
   __syncthreads();
 
-  const float* __restrict__ t0s = reinterpret_cast<const float*>(g.t0_smp);
+  const float* __restrict__ t0s = t0v;
   const int n_chunks = (n_rx + TJC - 1) / TJC;
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
@@ -243,8 +266,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     const int* map = g.rx_map + (int64_t)e * n_rx;
     for (int j = tid; j < n_rx; j += TTHREADS) {
       const int m = IDMAP ? j : map[j];
-      float rlo, rhi;
-      rx_bounds(m, rlo, rhi);
+      const float rlo = rmin[m], rhi = rmax[m];
       const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
       const int hi = (int)floorf(hi_e + rhi) + 4;
       const int len = min((hi - ws + 3) & ~3, W);  // host guarantees <= W
@@ -259,17 +281,39 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 8
   const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
   const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
-  auto issue_loads = [&](int q, const Cursor& cu) {
+  auto issue_loads = [&](int slot, int tslot, const Cursor& cu) {
     const int j = cu.cb * TJC + ld_jj;
     if (j >= n_rx) return;
-    const int2 mm = meta[(cu.T % 3) * n_rx + j];
+    const int2 mm = meta[tslot * n_rx + j];
     const int len = mm.x & 0x1fff;
-    const uint32_t wb = win_s + (uint32_t)(((q % NST) * TJC + ld_jj) * W + ld_o) * 4u;
+    const uint32_t wb = win_s + (uint32_t)((slot * TJC + ld_jj) * W + ld_o) * 4u;
     // K = wb0 - 4*(M_bits + ws) mod 2^32, so (wb0 - K)/4 = (M_bits + ws) mod 2^30
     const int ws = (int)((wb - (uint32_t)ld_o * 4u - (uint32_t)mm.y) >> 2) -
                    (kMagicBits & 0x3fffffff);
     const float* tr = a.rf + (int64_t)(f_begin + cu.fl) * a.rf_stride +
                       ((int64_t)cu.e * n_rx + cu.cb * TJC) * n_s + ld_trace;
+    if (ws >= 0 && ws + len <= n_s) {
+      // whole window inside the trace (the common case): one source pointer,
+      // copies at immediate +64 B steps
+      const float* p = tr + ws;
+      const int nc = (len - ld_o + 15) >> 4;  // this thread's copies
+      asm volatile(
+          "{\n .reg .pred q<8>;\n"
+          " setp.gt.s32 q0, %2, 0;\n setp.gt.s32 q1, %2, 1;\n setp.gt.s32 q2, %2, 2;\n"
+          " setp.gt.s32 q3, %2, 3;\n setp.gt.s32 q4, %2, 4;\n setp.gt.s32 q5, %2, 5;\n"
+          " setp.gt.s32 q6, %2, 6;\n setp.gt.s32 q7, %2, 7;\n"
+          " @q0 cp.async.cg.shared.global [%0], [%1], 16;\n"
+          " @q1 cp.async.cg.shared.global [%0+64], [%1+64], 16;\n"
+          " @q2 cp.async.cg.shared.global [%0+128], [%1+128], 16;\n"
+          " @q3 cp.async.cg.shared.global [%0+192], [%1+192], 16;\n"
+          " @q4 cp.async.cg.shared.global [%0+256], [%1+256], 16;\n"
+          " @q5 cp.async.cg.shared.global [%0+320], [%1+320], 16;\n"
+          " @q6 cp.async.cg.shared.global [%0+384], [%1+384], 16;\n"
+          " @q7 cp.async.cg.shared.global [%0+448], [%1+448], 16;\n}\n" ::"r"(wb),
+          "l"(p), "r"(nc)
+          : "memory");
+      return;
+    }
     // all 8 copies from distinct address registers (no write-after-read
     // stall on a register an in-flight cp.async still reads)
     const float* src[8];
@@ -303,13 +347,21 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   // barrier both publishes chunk q and retires chunk q-1, whose buffer
   // ((q+2) % 3) is then refilled with chunk q+2.
   Cursor cur{0, 0, 0, 0}, nx2{0, 0, 0, 0};
+  int slot_cur = 0, slot_ld = 0, tslot_cur = 0, tslot_ld = 0;  // q, q+2 and their T, mod 3
+  auto bump3 = [](int& x) { x = x == 2 ? 0 : x + 1; };
+  auto advance = [&](Cursor& cu, int& slot, int& tslot) {
+    const int t_prev = cu.T;
+    cu.next(n_chunks, n_tx);
+    bump3(slot);
+    if (cu.T != t_prev) bump3(tslot);
+  };
   make_meta(0);
   if (n_T > 1) make_meta(1);
   __syncthreads();
   for (int p = 0; p < 2; ++p) {
-    if (p < Q) issue_loads(p, nx2);
+    if (p < Q) issue_loads(slot_ld, tslot_ld, nx2);
     cp_async_commit();
-    nx2.next(n_chunks, n_tx);
+    advance(nx2, slot_ld, tslot_ld);
   }
 
   const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
@@ -324,25 +376,21 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       make_meta(cur.T + 2);  // ring slot of transmit T-1: retired
       if (n_chunks < 2) __syncthreads();  // first used by this iteration's loads
     }
-    if (q + 2 < Q) issue_loads(q + 2, nx2);
+    if (q + 2 < Q) issue_loads(slot_ld, tslot_ld, nx2);
     cp_async_commit();
-    nx2.next(n_chunks, n_tx);
+    advance(nx2, slot_ld, tslot_ld);
     if (cur.cb == 0) {
       if (PW) {
-        const float ca = reinterpret_cast<const float*>(g.cos_a)[cur.e];
-        const float sa = reinterpret_cast<const float*>(g.sin_a)[cur.e];
-        const float xs = O::mul(pxd, sa);
-        const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
-        const float tB = PAIR ? O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c)) : tA;
-        txd = L::make(tA, tB);
+        const u64 tt = txd_s[cur.e * TTHREADS + tid];
+        txd = PAIR ? (VT)tt : L::make(lo_f(tt), 0.0f);
       } else if (PAIR) {
-        txd = (VT)tm_ld2(tlane + 2 * g.tx_elements[cur.e]);
+        txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
       } else {
-        txd = L::make(tm_ld1(tlane + g.tx_elements[cur.e]), 0.0f);
+        txd = L::make(tm_ld1(tlane + txe[cur.e]), 0.0f);
       }
       t0e2 = L::splat(t0s[cur.e]);
     }
-    const int2* M = meta + (cur.T % 3) * n_rx + cur.cb * TJC;
+    const int2* M = meta + tslot_cur * n_rx + cur.cb * TJC;
     const int jn = min(TJC, n_rx - cur.cb * TJC);
 
     // one channel: rxd = receive delay(s), K = gather address base
@@ -411,7 +459,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       }
       acc = L::splat(0.0f);
     }
-    cur.next(n_chunks, n_tx);
+    advance(cur, slot_cur, tslot_cur);
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 
@@ -423,9 +471,11 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
 }
 
 static size_t tmem_smem_bytes(const bm_das_geometry& g, int W) {
-  size_t b = 16 + (size_t)g.n_tx * 8;
+  size_t b = 16 + (size_t)g.n_tx * 16;
+  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_elements * 8;
   b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 24;
   b = (b + 15) & ~size_t(15);
+  if (g.scheme == BM_PW) b += (size_t)g.n_tx * TTHREADS * 8;
   return b + (size_t)NST * TJC * W * 4;
 }
 
