@@ -281,9 +281,12 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 8
   const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
   const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
-  auto issue_loads = [&](int slot, int tslot, const Cursor& cu) {
+  // returns the fast path's source pointer, which the caller keeps live
+  // until the end of the iteration so that no instruction overwrites a
+  // register an in-flight cp.async still reads (a write-after-read stall)
+  auto issue_loads = [&](int slot, int tslot, const Cursor& cu) -> const float* {
     const int j = cu.cb * TJC + ld_jj;
-    if (j >= n_rx) return;
+    if (j >= n_rx) return nullptr;
     const int2 mm = meta[tslot * n_rx + j];
     const int len = mm.x & 0x1fff;
     const uint32_t wb = win_s + (uint32_t)((slot * TJC + ld_jj) * W + ld_o) * 4u;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
           " @q7 cp.async.cg.shared.global [%0+448], [%1+448], 16;\n}\n" ::"r"(wb),
           "l"(p), "r"(nc)
           : "memory");
-      return;
+      return p;
     }
     // all 8 copies from distinct address registers (no write-after-read
     // stall on a register an in-flight cp.async still reads)
@@ -341,6 +344,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
           "r"(nb[h + 1]), "r"(nb[h + 2]), "r"(nb[h + 3]), "r"(act[h]), "r"(act[h + 1]),
           "r"(act[h + 2]), "r"(act[h + 3])
           : "memory");
+    return nullptr;
   };
 
   // 3-stage cp.async pipeline, one barrier per chunk: at iteration q the
@@ -376,7 +380,8 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       make_meta(cur.T + 2);  // ring slot of transmit T-1: retired
       if (n_chunks < 2) __syncthreads();  // first used by this iteration's loads
     }
-    if (q + 2 < Q) issue_loads(slot_ld, tslot_ld, nx2);
+    const float* keep = nullptr;
+    if (q + 2 < Q) keep = issue_loads(slot_ld, tslot_ld, nx2);
     cp_async_commit();
     advance(nx2, slot_ld, tslot_ld);
     if (cur.cb == 0) {
@@ -460,6 +465,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       acc = L::splat(0.0f);
     }
     advance(cur, slot_cur, tslot_cur);
+    asm volatile("" ::"l"(keep));
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 
