@@ -367,8 +367,8 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->rx_identity = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   double zext = 0.0, xext = 0.0;
-  // the largest tile of either fast kernel (16 x 16 pixels) bounds both
-  const int TZM = 16, TXM = 16;
+  // the largest tile of the fast kernels (16 x 24 pixels) bounds them all
+  const int TZM = 16, TXM = 24;
   for (int i = 0; i < g->n_z; i += TZM) {
     const int l = (i + TZM < g->n_z ? i + TZM : g->n_z) - 1;
     zext = fmax(zext, z[l] - z[i]);

@@ -24,7 +24,7 @@
 
 namespace bm {
 
-constexpr int TX = 16, TTHREADS = 128, TJC = 32, NST = 3;
+constexpr int TX = 16, TJC = 32, NST = 3;
 
 struct TmemArgs {
   bm_das_geometry g;
@@ -136,11 +136,17 @@ __device__ __forceinline__ void tm_ld32f(uint32_t taddr, float (&d)[32]) {
 // PAIR: tile 16 x 16, thread = pixel pair (r, c) / (r + 4, c), TMEM columns 2m, 2m+1.
 // !PAIR: tile 8 x 16, thread = one pixel, TMEM column m, 4 CTAs per SM fit in TMEM.
 // Either way a warp's 32 gathers of one channel cover a 4 x 8 pixel block.
-template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP>
-__global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const TmemArgs a) {
+// HYB (pair only): a 6-warp CTA whose warps 4-5 keep their delay table in
+// SHARED memory next to the four TMEM warps -- TMEM caps the SM at 8 warps,
+// TMEM + SMEM together hold 12.  Tile 16 x 24 (warps 4-5: columns 16-23).
+template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP, bool HYB>
+__global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel(const TmemArgs a) {
   using O = R<float>;
   using L = Lane<PAIR>;
   typedef typename L::T VT;
+  constexpr int NTH = HYB ? 192 : 128;
+  constexpr int TXk = HYB ? 24 : TX;
+  constexpr bool TXD_SMEM = PW && !HYB;  // precomputed PW transmit delays
   constexpr int TZk = PAIR ? 16 : 8;
   constexpr int CPE = PAIR ? 2 : 1;  // TMEM columns per element
   const bm_das_geometry& g = a.g;
@@ -154,7 +160,8 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   const int off_rmin = (off_tmin + 16 * n_tx + 15) & ~15;
   const int off_meta = (off_rmin + 8 * n_el + 15) & ~15;
   const int off_txd = (off_meta + 24 * n_rx + 15) & ~15;
-  const int off_win = off_txd + (PW ? n_tx * TTHREADS * (int)sizeof(u64) : 0);
+  const int off_dsm = off_txd + (TXD_SMEM ? n_tx * NTH * (int)sizeof(u64) : 0);
+  const int off_win = off_dsm + (HYB ? n_el * 64 * (int)sizeof(u64) : 0);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
   float* tmin = reinterpret_cast<float*>(smem_raw + off_tmin);  // [n_tx]
   float* tmax = tmin + n_tx;                                    // [n_tx]
@@ -163,15 +170,20 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   float* rmin = reinterpret_cast<float*>(smem_raw + off_rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
   int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [3][n_rx]
-  u64* txd_s = reinterpret_cast<u64*>(smem_raw + off_txd);      // PW: [n_tx][128]
+  u64* txd_s = reinterpret_cast<u64*>(smem_raw + off_txd);      // PW: [n_tx][NTH]
+  u64* dsm = reinterpret_cast<u64*>(smem_raw + off_dsm);        // HYB: [n_el][64] pairs
   float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [NST][TJC][W]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int tiles_x = (g.n_x + TX - 1) / TX;
-  const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TX;
-  const int col = tx0 + (warp & 1) * 8 + (lane & 7);
-  const int rowA = tz0 + (warp >> 1) * (PAIR ? 8 : 4) + (lane >> 3), rowB = rowA + 4;
+  const int tiles_x = (g.n_x + TXk - 1) / TXk;
+  const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TXk;
+  const bool tm_warp = !HYB || warp < 4;  // delay table in TMEM (else shared memory)
+  const int wcol = tm_warp ? (warp & 1) * 8 : 16;
+  const int wrow = tm_warp ? (warp >> 1) * (PAIR ? 8 : 4) : (warp - 4) * 8;
+  const int col = tx0 + wcol + (lane & 7);
+  const int rowA = tz0 + wrow + (lane >> 3), rowB = rowA + 4;
+  const int dtid = tid - 128;  // HYB warps 4-5: row of the shared-memory table
   const int colc = min(col, g.n_x - 1);
   const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
 
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   __syncthreads();
   tm_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
+  const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
 
   // ---- exact receive delays of the thread's pixel(s) -> TMEM
   for (int m = 0; m < n_el; ++m) {
@@ -199,15 +211,18 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
     if (PAIR) {
       const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
-      tm_st2(tlane + 2 * m, dA, dB);
+      if (tm_warp)
+        tm_st2(tlane + 2 * m, dA, dB);
+      else
+        dsm[m * 64 + dtid] = pk(dA, dB);
     } else {
       tm_st1(tlane + m, dA);
     }
   }
-  tm_wait_st();
+  if (tm_warp) tm_wait_st();
 
   const int zl = min(tz0 + TZk, g.n_z) - 1;
-  const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TX, g.n_x) - 1];
+  const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TXk, g.n_x) - 1];
   const double z0 = g.z_pos[tz0], z1 = g.z_pos[zl];
   const double k = g.sampling_frequency / g.speed_of_sound;
   // receive-path delay bounds of element m over the tile rectangle (samples)
@@ -220,8 +235,8 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     lo = kf * sqrtf(dmin * dmin + z0f * z0f);
     hi = kf * sqrtf(dmax * dmax + z1f * z1f);
   };
-  for (int m = tid; m < n_el; m += TTHREADS) rx_bounds(m, rmin[m], rmax[m]);
-  for (int e = tid; e < n_tx; e += TTHREADS) {
+  for (int m = tid; m < n_el; m += NTH) rx_bounds(m, rmin[m], rmax[m]);
+  for (int e = tid; e < n_tx; e += NTH) {
     t0v[e] = reinterpret_cast<const float*>(g.t0_smp)[e];
     if (!PW) txe[e] = g.tx_elements[e];
     if (PW) {
@@ -235,16 +250,23 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
     }
   }
-  if (PW) {
-    // exact transmit delays fs*((z cos + x sin)/c) of the thread's pixels for
-    // every angle, once per CTA (beamform.py:218-225)
+  auto pw_txd = [&](int e) -> VT {  // fs*((z cos + x sin)/c), beamform.py:218-225
+    const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
+    const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+    const float xs = O::mul(pxd, sa);
+    const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+    const float tB = PAIR ? O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c)) : tA;
+    return L::make(tA, tB);
+  };
+  if (TXD_SMEM) {
+    // exact transmit delays of the thread's pixels for every angle, once per CTA
     for (int e = 0; e < n_tx; ++e) {
       const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
       const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
       const float xs = O::mul(pxd, sa);
       const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
       const float tB = PAIR ? O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c)) : tA;
-      txd_s[e * TTHREADS + tid] = pk(tA, tB);
+      txd_s[e * NTH + tid] = pk(tA, tB);
     }
   }
   __syncthreads();
@@ -264,7 +286,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     const float t0 = t0s[e];
     const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
     const int* map = g.rx_map + (int64_t)e * n_rx;
-    for (int j = tid; j < n_rx; j += TTHREADS) {
+    for (int j = tid; j < n_rx; j += NTH) {
       const int m = IDMAP ? j : map[j];
       const float rlo = rmin[m], rhi = rmax[m];
       const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
@@ -286,7 +308,7 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   // register an in-flight cp.async still reads (a write-after-read stall)
   auto issue_loads = [&](int slot, int tslot, const Cursor& cu) -> const float* {
     const int j = cu.cb * TJC + ld_jj;
-    if (j >= n_rx) return nullptr;
+    if ((HYB && tid >= 128) || j >= n_rx) return nullptr;
     const int2 mm = meta[tslot * n_rx + j];
     const int len = mm.x & 0x1fff;
     const uint32_t wb = win_s + (uint32_t)((slot * TJC + ld_jj) * W + ld_o) * 4u;
@@ -385,11 +407,16 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
     cp_async_commit();
     advance(nx2, slot_ld, tslot_ld);
     if (cur.cb == 0) {
-      if (PW) {
-        const u64 tt = txd_s[cur.e * TTHREADS + tid];
+      if (TXD_SMEM) {
+        const u64 tt = txd_s[cur.e * NTH + tid];
         txd = PAIR ? (VT)tt : L::make(lo_f(tt), 0.0f);
+      } else if (PW) {
+        txd = pw_txd(cur.e);
       } else if (PAIR) {
-        txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
+        if (tm_warp)
+          txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
+        else
+          txd = (VT)dsm[txe[cur.e] * 64 + dtid];
       } else {
         txd = L::make(tm_ld1(tlane + txe[cur.e]), 0.0f);
       }
@@ -430,7 +457,12 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
 #pragma unroll
         for (int h = 0; h < TJC; h += 16) {
           u64 d[16];
-          tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
+          if (tm_warp) {
+            tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = dsm[(cur.cb * TJC + h + i) * 64 + dtid];
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) channel((VT)d[i], (uint32_t)M[h + i].y);
         }
@@ -444,7 +476,11 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
       for (int jj = 0; jj < jn; ++jj) {
         const int2 mm = M[jj];
         const uint32_t col_m = CPE * ((unsigned)mm.x >> 13);
-        const VT rxd = PAIR ? (VT)tm_ld2(tlane + col_m) : L::make(tm_ld1(tlane + col_m), 0.0f);
+        VT rxd;
+        if (!tm_warp)
+          rxd = (VT)dsm[((unsigned)mm.x >> 13) * 64 + dtid];
+        else
+          rxd = PAIR ? (VT)tm_ld2(tlane + col_m) : L::make(tm_ld1(tlane + col_m), 0.0f);
         channel(rxd, (uint32_t)mm.y);
       }
     }
@@ -476,12 +512,17 @@ __global__ void __launch_bounds__(TTHREADS, PAIR ? 2 : 4) das_tmem_kernel(const 
   if (warp == 0) tm_dealloc(tbase, (uint32_t)a.tmem_cols);
 }
 
-static size_t tmem_smem_bytes(const bm_das_geometry& g, int W) {
+// variant of the TMEM kernel a launch uses
+enum TmemVariant { kScalar = 0, kPair = 1, kHybrid = 2 };
+
+static size_t tmem_smem_bytes(const bm_das_geometry& g, int W, int variant) {
+  const int nth = variant == kHybrid ? 192 : 128;
   size_t b = 16 + (size_t)g.n_tx * 16;
   b = ((b + 15) & ~size_t(15)) + (size_t)g.n_elements * 8;
   b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 24;
   b = (b + 15) & ~size_t(15);
-  if (g.scheme == BM_PW) b += (size_t)g.n_tx * TTHREADS * 8;
+  if (g.scheme == BM_PW && variant != kHybrid) b += (size_t)g.n_tx * nth * 8;
+  if (variant == kHybrid) b += (size_t)g.n_elements * 64 * 8;
   return b + (size_t)NST * TJC * W * 4;
 }
 
@@ -491,35 +532,40 @@ static int tmem_cols_for(int n_el, bool pair) {
   return cols;
 }
 
+// BM_DAS_LANES = hybrid (default when it fits) | pair | scalar
+static int tmem_variant(const bm_das_geometry& g) {
+  const char* e = getenv("BM_DAS_LANES");
+  const bool pair_ok = 2 * g.n_elements <= 512;
+  const bool hyb_ok = 2 * g.n_elements <= 256 &&
+                      tmem_smem_bytes(g, g.window_hint, kHybrid) + 1024 <= (227 * 1024) / 2;
+  if (e && !strcmp(e, "scalar")) return kScalar;
+  if (e && !strcmp(e, "pair")) return pair_ok ? kPair : kScalar;
+  if (hyb_ok) return kHybrid;
+  return pair_ok ? kPair : kScalar;
+}
+
 int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
   if (g.window_hint > 128) return 0;              // loader: <= 8 copies of 16 B per thread
   if (g.n_elements > 512) return 0;              // one TMEM column per element (scalar)
-  if (tmem_smem_bytes(g, g.window_hint) > 110 * 1024) return 0;
+  if (tmem_smem_bytes(g, g.window_hint, tmem_variant(g)) > 110 * 1024) return 0;
   return 1;
-}
-
-// BM_DAS_LANES = pair (default) | scalar: pixels per thread in the TMEM kernel
-static bool tmem_pair_choice(const bm_das_geometry& g) {
-  const char* e = getenv("BM_DAS_LANES");
-  if (e && !strcmp(e, "scalar")) return false;
-  if (e && !strcmp(e, "pair")) return 2 * g.n_elements <= 512;
-  return 2 * g.n_elements <= 512;
 }
 
 int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                     int64_t out_stride, int n_frames, cudaStream_t s) {
-  const bool pair = tmem_pair_choice(g);
+  const int variant = tmem_variant(g);
+  const bool pair = variant != kScalar, hyb = variant == kHybrid;
   TmemArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1,
              g.window_hint, tmem_cols_for(g.n_elements, pair)};
-  const int tz = pair ? 16 : 8;
-  const int tiles = ((g.n_z + tz - 1) / tz) * ((g.n_x + TX - 1) / TX);
+  const int tz = pair ? 16 : 8, tx = hyb ? 24 : TX, nth = hyb ? 192 : 128;
+  const int tiles = ((g.n_z + tz - 1) / tz) * ((g.n_x + tx - 1) / tx);
   // CTAs per SM are limited to what TMEM holds (512 columns): request enough
   // shared memory that no extra CTA is scheduled to spin in tcgen05.alloc
   int per_sm = 512 / a.tmem_cols;
   if (per_sm > 4) per_sm = 4;
-  size_t smem = tmem_smem_bytes(g, a.W);
+  size_t smem = tmem_smem_bytes(g, a.W, variant);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   if (smem < cap) smem = cap;
   // frames per CTA: amortise the per-CTA delay-table build over a frame
@@ -531,23 +577,31 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   a.frames_per_cta = fpc;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const TmemArgs);
-#define BM_TMEM_ROW(P)                                                                       \
-  das_tmem_kernel<P, false, false, false, false>, das_tmem_kernel<P, false, false, false, true>, \
-      das_tmem_kernel<P, false, false, true, false>, das_tmem_kernel<P, false, false, true, true>, \
-      das_tmem_kernel<P, false, true, false, false>, das_tmem_kernel<P, false, true, false, true>, \
-      das_tmem_kernel<P, false, true, true, false>, das_tmem_kernel<P, false, true, true, true>,   \
-      das_tmem_kernel<P, true, false, false, false>, das_tmem_kernel<P, true, false, false, true>, \
-      das_tmem_kernel<P, true, false, true, false>, das_tmem_kernel<P, true, false, true, true>,   \
-      das_tmem_kernel<P, true, true, false, false>, das_tmem_kernel<P, true, true, false, true>,   \
-      das_tmem_kernel<P, true, true, true, false>, das_tmem_kernel<P, true, true, true, true>
-  static const kfn table[32] = {BM_TMEM_ROW(false), BM_TMEM_ROW(true)};
+#define BM_TMEM_ROW(P, H)                                                                    \
+  das_tmem_kernel<P, false, false, false, false, H>,                                        \
+      das_tmem_kernel<P, false, false, false, true, H>,                                     \
+      das_tmem_kernel<P, false, false, true, false, H>,                                     \
+      das_tmem_kernel<P, false, false, true, true, H>,                                      \
+      das_tmem_kernel<P, false, true, false, false, H>,                                     \
+      das_tmem_kernel<P, false, true, false, true, H>,                                      \
+      das_tmem_kernel<P, false, true, true, false, H>,                                      \
+      das_tmem_kernel<P, false, true, true, true, H>,                                       \
+      das_tmem_kernel<P, true, false, false, false, H>,                                     \
+      das_tmem_kernel<P, true, false, false, true, H>,                                      \
+      das_tmem_kernel<P, true, false, true, false, H>,                                      \
+      das_tmem_kernel<P, true, false, true, true, H>,                                       \
+      das_tmem_kernel<P, true, true, false, false, H>,                                      \
+      das_tmem_kernel<P, true, true, false, true, H>,                                       \
+      das_tmem_kernel<P, true, true, true, false, H>, das_tmem_kernel<P, true, true, true, true, H>
+  static const kfn table[48] = {BM_TMEM_ROW(false, false), BM_TMEM_ROW(true, false),
+                                BM_TMEM_ROW(true, true)};
 #undef BM_TMEM_ROW
-  const kfn k = table[(pair ? 16 : 0) | (pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
-                      (g.rx_identity ? 1 : 0)];
+  const kfn k = table[16 * variant + ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
+                                      (g.rx_identity ? 1 : 0))];
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
-  k<<<grid, TTHREADS, smem, s>>>(a);
+  k<<<grid, nth, smem, s>>>(a);
   return cuda_status();
 }
 
