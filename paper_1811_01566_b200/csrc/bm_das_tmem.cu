@@ -140,7 +140,7 @@ __device__ __forceinline__ void tm_ld32f(uint32_t taddr, float (&d)[32]) {
 // SHARED memory next to the four TMEM warps -- TMEM caps the SM at 8 warps,
 // TMEM + SMEM together hold 12.  Tile 16 x 24 (warps 4-5: columns 16-23).
 template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP, bool HYB>
-__global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel(const TmemArgs a) {
+__global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 1 : 4) das_tmem_kernel(const TmemArgs a) {
   using O = R<float>;
   using L = Lane<PAIR>;
   typedef typename L::T VT;

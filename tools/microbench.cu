@@ -47,7 +47,7 @@ __global__ void bench(int salt) {
   }
   const u64 one = 0x3f8000003f800000ull;
   __syncthreads();
-  const long long t0 = clock64();
+  long long t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -60,6 +60,11 @@ __global__ void bench(int salt) {
         f[i] += x;
         addr[i] ^= 4u;
       }
+      if (KIND == 5) {                                              // LDS.32, 1 address
+        float x;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[0] & ~127u));
+        f[i] += x;
+      }
       if (KIND == 4) {                                              // LDS.64
         u64 x;
         asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x) : "r"(addr[i] & ~7u));
@@ -68,6 +73,7 @@ __global__ void bench(int salt) {
       }
     }
   }
+  __syncthreads();  // the slowest warp ends the interval
   const long long t1 = clock64();
   u64 acc = 0;
   for (int i = 0; i < 8; ++i) acc ^= v[i] ^ (u64)__float_as_uint(f[i]);
@@ -78,13 +84,13 @@ __global__ void bench(int salt) {
 int main() {
   int dev = 0, sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const char* names[5] = {"fadd2", "fadd", "ffma2_rz", "lds32_gather", "lds64"};
+  const char* names[6] = {"fadd2", "fadd", "ffma2_rz", "lds32_gather", "lds64", "lds32_bcast"};
   printf("{\"sm_count\": %d", sms);
-  for (int kind = 0; kind < 5; ++kind) {
+  for (int kind = 0; kind < 6; ++kind) {
     for (int warps : {4, 8, 16}) {
       const int threads = 32 * warps;
       auto fn = kind == 0 ? bench<0> : kind == 1 ? bench<1> : kind == 2 ? bench<2>
-               : kind == 3 ? bench<3> : bench<4>;
+               : kind == 3 ? bench<3> : kind == 4 ? bench<4> : bench<5>;
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
       fn<<<sms, threads, 32768>>>(1);
       fn<<<sms, threads, 32768>>>(2);
