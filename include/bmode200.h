@@ -71,11 +71,13 @@ typedef struct bm_das_geometry {
   int32_t n_elements; /* probe elements                                      */
   int32_t n_z;        /* image rows (depth)                                  */
   int32_t n_x;        /* image columns (lateral)                             */
-  int32_t window_hint; /* set by bm_das_prepare: max samples a fast-path tile
+  int32_t window_hint; /* set by bm_das_prepare: max samples a 16 x 16-pixel tile's
                           window can span (0 = not prepared -> generic kernel) */
   int32_t t0_nonzero;  /* set by bm_das_prepare: 1 if any fs*t0 != 0 (the fast
                           kernel then keeps the reference's "- t0" rounding step) */
   int32_t rx_identity; /* set by bm_das_prepare: 1 if rx_map[e][j] == j for all e, j */
+  int32_t window_hint_wide; /* set by bm_das_prepare: window bound of 16 x 24 tiles */
+  int32_t reserved;
   double speed_of_sound;     /* c  (cast to dtype, beamform.py:206)          */
   double sampling_frequency; /* fs (cast to dtype, beamform.py:207)          */
   const double* elem_x;      /* [n_elements] element centres, f64            */

@@ -363,24 +363,28 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
                               const double* z, const double* t0_smp, const int32_t* rx_map) {
   if (!g || !elem_x || !x || !z || !t0_smp || !rx_map) return BM_ERR_INVALID_ARGUMENT;
   g->window_hint = 0;
+  g->window_hint_wide = 0;
   g->t0_nonzero = 1;
   g->rx_identity = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
-  double zext = 0.0, xext = 0.0;
-  // the largest tile of the fast kernels (16 x 24 pixels) bounds them all
-  const int TZM = 16, TXM = 24;
-  for (int i = 0; i < g->n_z; i += TZM) {
-    const int l = (i + TZM < g->n_z ? i + TZM : g->n_z) - 1;
-    zext = fmax(zext, z[l] - z[i]);
-  }
-  for (int i = 0; i < g->n_x; i += TXM) {
-    const int l = (i + TXM < g->n_x ? i + TXM : g->n_x) - 1;
-    xext = fmax(xext, x[l] - x[i]);
-  }
+  // window bound of a tz x tx-pixel tile: tx delay range + rx delay range
+  // (each <= k * tile diagonal) + margins
   const double k = g->sampling_frequency / g->speed_of_sound;
-  const double diag = sqrt(zext * zext + xext * xext);
-  int W = (int)ceil(2.0 * k * diag + 16.0);
-  W = (W + 3) & ~3;
+  auto bound = [&](int tz, int tx) {
+    double zext = 0.0, xext = 0.0;
+    for (int i = 0; i < g->n_z; i += tz) {
+      const int l = (i + tz < g->n_z ? i + tz : g->n_z) - 1;
+      zext = fmax(zext, z[l] - z[i]);
+    }
+    for (int i = 0; i < g->n_x; i += tx) {
+      const int l = (i + tx < g->n_x ? i + tx : g->n_x) - 1;
+      xext = fmax(xext, x[l] - x[i]);
+    }
+    const int w = (int)ceil(2.0 * k * sqrt(zext * zext + xext * xext) + 16.0);
+    return (w + 3) & ~3;
+  };
+  int W = bound(16, 16);
+  const int W_wide = bound(16, 24);
   // largest |t|: every delay is <= k * (farthest grid corner from any element
   // or from the origin) per path
   double dmax = 0.0;
@@ -405,7 +409,8 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
     if (rx_map[i] != (int)(i % g->n_rx)) ident = 0;
   g->rx_identity = ident;
   if (!(tabs < 4194304.0)) return BM_OK;  // outside the exact magic-number range
-  if (W > 4096) return BM_OK;
+  if (W_wide > 4096) return BM_OK;
   g->window_hint = W;
+  g->window_hint_wide = W_wide;
   return BM_OK;
 }

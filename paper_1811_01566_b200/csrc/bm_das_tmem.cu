@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
     }
   };
   // cp.async staging: 4 threads per channel, 16 B copies at fixed slots
-  // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 8
+  // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 16
   const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
   const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
   // returns the fast path's source pointer, which the caller keeps live
@@ -337,35 +337,55 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
           " @q7 cp.async.cg.shared.global [%0+448], [%1+448], 16;\n}\n" ::"r"(wb),
           "l"(p), "r"(nc)
           : "memory");
+      if (nc > 8)  // windows of 129-256 samples
+        asm volatile(
+            "{\n .reg .pred q<8>;\n"
+            " setp.gt.s32 q0, %2, 8;\n setp.gt.s32 q1, %2, 9;\n setp.gt.s32 q2, %2, 10;\n"
+            " setp.gt.s32 q3, %2, 11;\n setp.gt.s32 q4, %2, 12;\n setp.gt.s32 q5, %2, 13;\n"
+            " setp.gt.s32 q6, %2, 14;\n setp.gt.s32 q7, %2, 15;\n"
+            " @q0 cp.async.cg.shared.global [%0+512], [%1+512], 16;\n"
+            " @q1 cp.async.cg.shared.global [%0+576], [%1+576], 16;\n"
+            " @q2 cp.async.cg.shared.global [%0+640], [%1+640], 16;\n"
+            " @q3 cp.async.cg.shared.global [%0+704], [%1+704], 16;\n"
+            " @q4 cp.async.cg.shared.global [%0+768], [%1+768], 16;\n"
+            " @q5 cp.async.cg.shared.global [%0+832], [%1+832], 16;\n"
+            " @q6 cp.async.cg.shared.global [%0+896], [%1+896], 16;\n"
+            " @q7 cp.async.cg.shared.global [%0+960], [%1+960], 16;\n}\n" ::"r"(wb),
+            "l"(p), "r"(nc)
+            : "memory");
       return p;
     }
-    // all 8 copies from distinct address registers (no write-after-read
-    // stall on a register an in-flight cp.async still reads)
-    const float* src[8];
-    int nb[8], act[8];
+    // window crosses a trace end (rare): per-copy source and zero fill; the
+    // copies of each 8-block use distinct address registers
+    for (int i0 = 0; i0 < 16 && ld_o + 16 * i0 < len; i0 += 8) {
+      const float* src[8];
+      int nb[8], act[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int o = ld_o + 16 * i;
-      const bool in = (unsigned)(ws + o) <= (unsigned)(n_s - 4);
-      src[i] = tr + (in ? ws + 16 * i : -ld_o);
-      nb[i] = in ? 16 : 0;
-      act[i] = o < len;
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k;
+        const int o = ld_o + 16 * i;
+        const bool in = (unsigned)(ws + o) <= (unsigned)(n_s - 4);
+        src[k] = tr + (in ? ws + 16 * i : -ld_o);
+        nb[k] = in ? 16 : 0;
+        act[k] = o < len;
+      }
+      const uint32_t wbi = wb + 64u * i0;
+#pragma unroll
+      for (int h = 0; h < 8; h += 4)
+        asm volatile(
+            "{\n .reg .pred q0, q1, q2, q3;\n"
+            " setp.ne.b32 q0, %12, 0;\n setp.ne.b32 q1, %13, 0;\n"
+            " setp.ne.b32 q2, %14, 0;\n setp.ne.b32 q3, %15, 0;\n"
+            " @q0 cp.async.cg.shared.global [%0], [%4], 16, %8;\n"
+            " @q1 cp.async.cg.shared.global [%1], [%5], 16, %9;\n"
+            " @q2 cp.async.cg.shared.global [%2], [%6], 16, %10;\n"
+            " @q3 cp.async.cg.shared.global [%3], [%7], 16, %11;\n}\n" ::"r"(wbi + 64u * h),
+            "r"(wbi + 64u * (h + 1)), "r"(wbi + 64u * (h + 2)), "r"(wbi + 64u * (h + 3)),
+            "l"(src[h]), "l"(src[h + 1]), "l"(src[h + 2]), "l"(src[h + 3]), "r"(nb[h]),
+            "r"(nb[h + 1]), "r"(nb[h + 2]), "r"(nb[h + 3]), "r"(act[h]), "r"(act[h + 1]),
+            "r"(act[h + 2]), "r"(act[h + 3])
+            : "memory");
     }
-#pragma unroll
-    for (int h = 0; h < 8; h += 4)
-      asm volatile(
-          "{\n .reg .pred q0, q1, q2, q3;\n"
-          " setp.ne.b32 q0, %12, 0;\n setp.ne.b32 q1, %13, 0;\n"
-          " setp.ne.b32 q2, %14, 0;\n setp.ne.b32 q3, %15, 0;\n"
-          " @q0 cp.async.cg.shared.global [%0], [%4], 16, %8;\n"
-          " @q1 cp.async.cg.shared.global [%1], [%5], 16, %9;\n"
-          " @q2 cp.async.cg.shared.global [%2], [%6], 16, %10;\n"
-          " @q3 cp.async.cg.shared.global [%3], [%7], 16, %11;\n}\n" ::"r"(wb + 64u * h),
-          "r"(wb + 64u * (h + 1)), "r"(wb + 64u * (h + 2)), "r"(wb + 64u * (h + 3)),
-          "l"(src[h]), "l"(src[h + 1]), "l"(src[h + 2]), "l"(src[h + 3]), "r"(nb[h]),
-          "r"(nb[h + 1]), "r"(nb[h + 2]), "r"(nb[h + 3]), "r"(act[h]), "r"(act[h + 1]),
-          "r"(act[h + 2]), "r"(act[h + 3])
-          : "memory");
     return nullptr;
   };
 
@@ -537,8 +557,9 @@ static int tmem_cols_for(int n_el, bool pair) {
 static int tmem_variant(const bm_das_geometry& g) {
   const char* e = getenv("BM_DAS_LANES");
   const bool pair_ok = 2 * g.n_elements <= 512;
-  const bool hyb_ok = 2 * g.n_elements <= 256 &&
-                      tmem_smem_bytes(g, g.window_hint, kHybrid) + 1024 <= (227 * 1024) / 2;
+  const bool hyb_ok = 2 * g.n_elements <= 256 && g.window_hint_wide > 0 &&
+                      g.window_hint_wide <= 256 &&
+                      tmem_smem_bytes(g, g.window_hint_wide, kHybrid) + 1024 <= (227 * 1024) / 2;
   if (e && !strcmp(e, "scalar")) return kScalar;
   if (e && !strcmp(e, "hybrid") && hyb_ok) return kHybrid;
   return pair_ok ? kPair : kScalar;
@@ -547,7 +568,7 @@ static int tmem_variant(const bm_das_geometry& g) {
 int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
-  if (g.window_hint > 128) return 0;              // loader: <= 8 copies of 16 B per thread
+  if (g.window_hint > 256) return 0;             // loader: <= 16 copies of 16 B per thread
   if (g.n_elements > 512) return 0;              // one TMEM column per element (scalar)
   if (tmem_smem_bytes(g, g.window_hint, tmem_variant(g)) > 110 * 1024) return 0;
   return 1;
@@ -558,7 +579,7 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   const int variant = tmem_variant(g);
   const bool pair = variant != kScalar, hyb = variant == kHybrid;
   TmemArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1,
-             g.window_hint, tmem_cols_for(g.n_elements, pair)};
+             hyb ? g.window_hint_wide : g.window_hint, tmem_cols_for(g.n_elements, pair)};
   const int tz = pair ? 16 : 8, tx = hyb ? 24 : TX, nth = hyb ? 192 : 128;
   const int tiles = ((g.n_z + tz - 1) / tz) * ((g.n_x + tx - 1) / tx);
   // CTAs per SM are limited to what TMEM holds (512 columns): request enough

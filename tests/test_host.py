@@ -46,8 +46,8 @@ def test_library_contains_sm100a_code():
 
 
 def test_geometry_struct_layout():
-    # 14 int32 + 2 double + 10 pointers, no padding surprises
-    assert ctypes.sizeof(N.DasGeometry) == 14 * 4 + 2 * 8 + 10 * 8
+    # 16 int32 + 2 double + 10 pointers, no padding surprises
+    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8
 
 
 def test_invalid_arguments_rejected_without_gpu():
