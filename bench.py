@@ -332,16 +332,18 @@ def main():
     contrib = B * ctx.n_tx * ctx.n_elements * grid.n_z * grid.n_x
     sm_mhz = clk["sm_mhz"] or 1965.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Binding roof of DAS: the FP32 pipe.  The exact
-    # (bitwise) linear formulation is 9 FP32 lane-ops per contribution
-    # (t, floor, k0, a, 1-a, 2 rounded products, 2 adds; nearest: 4); the
-    # B200 FP32 pipe retires 128 lane-ops/clk/SM (profiles/r01_microbench.json:
-    # FADD2 = 2 warp-instr/clk/SM).  Shared-memory gathers (4 B each, 2 per
-    # contribution) run at 512 B/clk/SM (LDS.32 3.8 warp-instr/clk/SM), i.e.
-    # 64 contributions/clk/SM, far from binding; HBM is ~100x away.
+    # Rooflines of DAS, both measured on this B200
+    # (profiles/r01_microbench.json):
+    #  * FP32 pipe: the exact (bitwise) linear formulation is 9 FP32 lane-ops
+    #    per contribution (t, floor, k0, a, 1-a, 2 rounded products, 2 adds;
+    #    nearest: 4); FADD2/FFMA2 retire 2 warp-instr/clk/SM = 128 lane-ops.
+    #  * shared-memory gathers: 2 x 4 B per linear contribution (1 nearest);
+    #    LDS.32 retires 1 warp-instr/clk/SM = 128 B/clk/SM.
+    # The binding roof is the slower of the two; HBM is ~100x away.
     ops = 9 if args.interp == "linear" else 4
+    gb = 8 if args.interp == "linear" else 4
     t_fp32 = contrib * ops / (n_sm * 128 * sm_mhz * 1e6)
-    t_lds = contrib * 2 / (n_sm * 4 * 32 * sm_mhz * 1e6)
+    t_lds = contrib * gb / (n_sm * 128 * sm_mhz * 1e6)
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
@@ -350,14 +352,15 @@ def main():
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
         "note": "DAS is FP32-pipe bound, not HBM bound: see binding",
         "binding": {
-            "resource": "FP32 pipe (9 lane-ops per linear contribution, 128 lane-ops/clk/SM)",
+            "resource": ("FP32 pipe (9 lane-ops per linear contribution, 128 lane-ops/clk/SM); "
+                         "SMEM gather roof (8 B per contribution, 128 B/clk/SM) reported beside"),
             "contributions_per_launch": contrib,
             "achieved_gcontrib_s": round(contrib / (das_ms / 1000.0) / 1e9, 1),
             "achieved_tflops_fp32_lane_ops": round(contrib * ops / (das_ms / 1000.0) / 1e12, 2),
             "peak_tflops_fp32_lane_ops": round(n_sm * 128 * sm_mhz * 1e6 / 1e12, 2),
             "t_fp32_roof_ms": round(t_fp32 * 1000, 4),
             "t_smem_gather_roof_ms": round(t_lds * 1000, 4),
-            "frac": round(t_fp32 / (das_ms / 1000.0), 4),
+            "frac": round(max(t_fp32, t_lds) / (das_ms / 1000.0), 4),
             "sm_mhz": sm_mhz, "n_sm": n_sm},
     }
 

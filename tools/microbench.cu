@@ -56,18 +56,18 @@ __global__ void bench(int salt) {
       if (KIND == 2) v[i] = ffma2z(v[i], one);                      // FFMA2 (x*y + 0)
       if (KIND == 3) {                                              // LDS.32 gather
         float x;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[i]));
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[i]));
         f[i] += x;
         addr[i] ^= 4u;
       }
       if (KIND == 5) {                                              // LDS.32, 1 address
         float x;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[0] & ~127u));
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[0] & ~127u));
         f[i] += x;
       }
       if (KIND == 4) {                                              // LDS.64
         u64 x;
-        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x) : "r"(addr[i] & ~7u));
+        asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(x) : "r"(addr[i] & ~7u));
         v[i] ^= x;
         addr[i] ^= 8u;
       }
