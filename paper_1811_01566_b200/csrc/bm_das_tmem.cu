@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   const int off_tmin = 16;
   const int off_rmin = (off_tmin + 16 * n_tx + 15) & ~15;
   const int off_meta = (off_rmin + 8 * n_el + 15) & ~15;
-  const int off_txd = (off_meta + 24 * n_rx + 15) & ~15;
+  const int nrp = (n_rx + 3) & ~3;  // meta row stride (16 B aligned rows)
+  const int off_txd = off_meta + 24 * nrp;
   const int off_dsm = off_txd + (TXD_SMEM ? n_tx * NTH * (int)sizeof(u64) : 0);
   const int off_win = off_dsm + (HYB ? n_el * 64 * (int)sizeof(u64) : 0);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
   float* rmin = reinterpret_cast<float*>(smem_raw + off_rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
-  int2* meta = reinterpret_cast<int2*>(smem_raw + off_meta);    // [3][n_rx]
+  int* metaX = reinterpret_cast<int*>(smem_raw + off_meta);     // [3][nrp] len | m << 13
+  int* metaK = metaX + 3 * nrp;                                 // [3][nrp] gather base K
   u64* txd_s = reinterpret_cast<u64*>(smem_raw + off_txd);      // PW: [n_tx][NTH]
   u64* dsm = reinterpret_cast<u64*>(smem_raw + off_dsm);        // HYB: [n_el][64] pairs
   float* win = reinterpret_cast<float*>(smem_raw + off_win);    // [NST][TJC][W]
@@ -282,7 +284,8 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   //   x = staged length | element m << 13,  y = K (gather address base)
   auto make_meta = [&](int T) {
     const int e = T % n_tx;
-    int2* M = meta + (T % 3) * n_rx;
+    int* MX = metaX + (T % 3) * nrp;
+    int* MK = metaK + (T % 3) * nrp;
     const float t0 = t0s[e];
     const float lo_e = tmin[e] - t0, hi_e = tmax[e] - t0;
     const int* map = g.rx_map + (int64_t)e * n_rx;
@@ -296,7 +299,8 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       const int buf = (T * n_chunks + cb) % NST;
       const uint32_t K = win_s + (uint32_t)((buf * TJC + jj) * W) * 4u -
                          (uint32_t)(kMagicBits + ws) * 4u;
-      M[j] = make_int2(len | (m << 13), (int)K);
+      MX[j] = len | (m << 13);
+      MK[j] = (int)K;
     }
   };
   // cp.async staging: 4 threads per channel, 16 B copies at fixed slots
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   auto issue_loads = [&](int slot, int tslot, const Cursor& cu) -> const float* {
     const int j = cu.cb * TJC + ld_jj;
     if ((HYB && tid >= 128) || j >= n_rx) return nullptr;
-    const int2 mm = meta[tslot * n_rx + j];
+    const int2 mm = make_int2(metaX[tslot * nrp + j], metaK[tslot * nrp + j]);
     const int len = mm.x & 0x1fff;
     const uint32_t wb = win_s + (uint32_t)((slot * TJC + ld_jj) * W + ld_o) * 4u;
     // K = wb0 - 4*(M_bits + ws) mod 2^32, so (wb0 - K)/4 = (M_bits + ws) mod 2^30
@@ -442,7 +446,9 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       }
       t0e2 = L::splat(t0s[cur.e]);
     }
-    const int2* M = meta + tslot_cur * n_rx + cur.cb * TJC;
+    const int* MXc = metaX + tslot_cur * nrp + cur.cb * TJC;
+    const int* MKc = metaK + tslot_cur * nrp + cur.cb * TJC;
+    const int4* MK4 = reinterpret_cast<const int4*>(MKc);  // 4 gather bases per LDS.128
     const int jn = min(TJC, n_rx - cur.cb * TJC);
 
     // one channel: rxd = receive delay(s), K = gather address base
@@ -484,17 +490,29 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
             for (int i = 0; i < 16; ++i) d[i] = dsm[(cur.cb * TJC + h + i) * 64 + dtid];
           }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) channel((VT)d[i], (uint32_t)M[h + i].y);
+          for (int i = 0; i < 16; i += 4) {
+            const int4 k4 = MK4[(h + i) >> 2];
+            channel((VT)d[i], (uint32_t)k4.x);
+            channel((VT)d[i + 1], (uint32_t)k4.y);
+            channel((VT)d[i + 2], (uint32_t)k4.z);
+            channel((VT)d[i + 3], (uint32_t)k4.w);
+          }
         }
       } else {
         float d[32];
         tm_ld32f(tlane + cur.cb * TJC, d);
 #pragma unroll
-        for (int i = 0; i < TJC; ++i) channel(L::make(d[i], 0.0f), (uint32_t)M[i].y);
+        for (int i = 0; i < TJC; i += 4) {
+          const int4 k4 = MK4[i >> 2];
+          channel(L::make(d[i], 0.0f), (uint32_t)k4.x);
+          channel(L::make(d[i + 1], 0.0f), (uint32_t)k4.y);
+          channel(L::make(d[i + 2], 0.0f), (uint32_t)k4.z);
+          channel(L::make(d[i + 3], 0.0f), (uint32_t)k4.w);
+        }
       }
     } else {
       for (int jj = 0; jj < jn; ++jj) {
-        const int2 mm = M[jj];
+        const int2 mm = make_int2(MXc[jj], MKc[jj]);
         const uint32_t col_m = CPE * ((unsigned)mm.x >> 13);
         VT rxd;
         if (!tm_warp)
@@ -539,8 +557,7 @@ static size_t tmem_smem_bytes(const bm_das_geometry& g, int W, int variant) {
   const int nth = variant == kHybrid ? 192 : 128;
   size_t b = 16 + (size_t)g.n_tx * 16;
   b = ((b + 15) & ~size_t(15)) + (size_t)g.n_elements * 8;
-  b = ((b + 15) & ~size_t(15)) + (size_t)g.n_rx * 24;
-  b = (b + 15) & ~size_t(15);
+  b = ((b + 15) & ~size_t(15)) + (size_t)((g.n_rx + 3) & ~3) * 24;
   if (g.scheme == BM_PW && variant != kHybrid) b += (size_t)g.n_tx * nth * 8;
   if (variant == kHybrid) b += (size_t)g.n_elements * 64 * 8;
   return b + (size_t)NST * TJC * W * 4;
