@@ -111,6 +111,11 @@ int bm_das_prepare(bm_das_geometry* g, const double* elem_x_host, const double* 
                    const double* z_host, const double* t0_smp_host,
                    const int32_t* rx_map_host);
 
+/* Which DAS kernel bm_das_beamform would run for this geometry and frame
+ * stride: 0 generic, 1 shared-memory fast path, 2/3/4 tensor-memory fast path
+ * (scalar / pixel pair / hybrid), -1 invalid geometry.  Host only. */
+int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride);
+
 /* Delay-and-Sum of n_frames frames.
  *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride
  *   out: device dtype[n_frames][n_z][n_x],  frame f at out + f*out_frame_stride

@@ -168,6 +168,14 @@ class DasPlan:
         g.interp = N.BM_NEAREST if interp == "nearest" else N.BM_LINEAR
         return g
 
+    KERNELS = {0: "generic", 1: "smem", 2: "tmem-scalar", 3: "tmem-pair", 4: "tmem-hybrid"}
+
+    def kernel_for(self, n_samples: int, interp: str = "linear", fast: bool = True) -> str:
+        """Name of the CUDA kernel a launch with this trace length would use."""
+        g = self.geometry(n_samples, interp, fast)
+        stride = int(self._geom.n_tx) * int(self.n_rx) * int(n_samples)
+        return self.KERNELS.get(N.load().bm_das_select(ctypes.byref(g), stride), "invalid")
+
     def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True):
         """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
         ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``."""

@@ -56,6 +56,7 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
 int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                     int64_t out_stride, int n_frames, cudaStream_t s);
+int das_tmem_variant(const bm_das_geometry& g);  // 0 scalar, 1 pair, 2 hybrid
 
 // DAS kernel selection: BM_DAS_KERNEL = auto (default) | tmem | smem | generic
 inline int das_kernel_choice() {

@@ -233,6 +233,15 @@ extern "C" int bm_das_aperture_span(const bm_das_geometry* g, double f_number,
   return bm::cuda_status();
 }
 
+extern "C" int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride) {
+  if (bm::check_geometry(g)) return -1;
+  const int choice = bm::das_kernel_choice();
+  if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
+    return 2 + bm::das_tmem_variant(*g);
+  if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride)) return 1;
+  return 0;
+}
+
 extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
                                void* out, int64_t out_frame_stride, int32_t n_frames,
                                void* stream) {

@@ -582,6 +582,8 @@ static int tmem_variant(const bm_das_geometry& g) {
   return pair_ok ? kPair : kScalar;
 }
 
+int das_tmem_variant(const bm_das_geometry& g) { return tmem_variant(g); }
+
 int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0) return 0;
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;
