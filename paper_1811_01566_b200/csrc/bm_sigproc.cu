@@ -97,41 +97,42 @@ __global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict_
   }
   __syncthreads();
 
-  const int nb = half_n << log2L;  // butterflies per pass
-  for (int pass = 0; pass < 2; ++pass) {
-    const T sign = pass == 0 ? T(1) : T(-1);  // inverse: conjugate twiddles
-    for (int s = 1; s <= log2n; ++s) {
-      const int h = 1 << (s - 1);
-      for (int b = threadIdx.x; b < nb; b += nt) {
-        const int l = b >> (log2n - 1);
-        const int bb = b & (half_n - 1);
-        const int pos = bb & (h - 1);
-        const int i = ((bb >> (s - 1)) << s) + pos;
-        V w = tw[pos << (log2n - s)];
-        w.y *= sign;
-        V* lane = buf + (l << log2n);
-        const V u = lane[i];
-        const V t = cmul<T>(w, lane[i + h]);
-        lane[i] = V{u.x + t.x, u.y + t.y};
-        lane[i + h] = V{u.x - t.x, u.y - t.y};
+  // FFT -> gain -> bit reversal -> inverse FFT, one warp per lane: the
+  // passes only need warp-level synchronisation
+  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31, nwarps = nt >> 5;
+  for (int l = warp; l < L; l += nwarps) {
+    V* lane = buf + (l << log2n);
+    for (int pass = 0; pass < 2; ++pass) {
+      const T sign = pass == 0 ? T(1) : T(-1);  // inverse: conjugate twiddles
+      for (int s = 1; s <= log2n; ++s) {
+        const int h = 1 << (s - 1);
+        for (int bb = wl; bb < half_n; bb += 32) {
+          const int pos = bb & (h - 1);
+          const int i = ((bb >> (s - 1)) << s) + pos;
+          V w = tw[pos << (log2n - s)];
+          w.y *= sign;
+          const V u = lane[i];
+          const V t = cmul<T>(w, lane[i + h]);
+          lane[i] = V{u.x + t.x, u.y + t.y};
+          lane[i + h] = V{u.x - t.x, u.y - t.y};
+        }
+        __syncwarp();
       }
-      __syncthreads();
-    }
-    if (pass == 0) {
-      // one-sided gain, then bit-reverse permutation for the inverse DIT
-      for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
-        const int l = idx >> log2n, k = idx & (n - 1);
-        const int r = __brev(k) >> (32 - log2n);
-        if (k > r) continue;
-        V* lane = buf + (l << log2n);
-        const T gk = hilbert_gain<T>(k, n), gr = hilbert_gain<T>(r, n);
-        const V a = lane[k], bv = lane[r];
-        lane[k] = V{bv.x * gr, bv.y * gr};
-        lane[r] = V{a.x * gk, a.y * gk};
+      if (pass == 0) {
+        // one-sided gain, then bit-reverse permutation for the inverse DIT
+        for (int k = wl; k < n; k += 32) {
+          const int r = __brev(k) >> (32 - log2n);
+          if (k > r) continue;
+          const T gk = hilbert_gain<T>(k, n), gr = hilbert_gain<T>(r, n);
+          const V a = lane[k], bv = lane[r];
+          lane[k] = V{bv.x * gr, bv.y * gr};
+          lane[r] = V{a.x * gk, a.y * gk};
+        }
+        __syncwarp();
       }
-      __syncthreads();
     }
   }
+  __syncthreads();
 
   const T inv_n = T(1) / T(n);
   T vmax = T(0);
