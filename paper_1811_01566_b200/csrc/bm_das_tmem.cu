@@ -24,7 +24,7 @@
 
 namespace bm {
 
-constexpr int TX = 16, TJC = 32, NST = 3;
+constexpr int TX = 16, NST = 3;  // channels per chunk (32 or 64) is a launch argument
 
 struct TmemArgs {
   bm_das_geometry g;
@@ -36,6 +36,7 @@ struct TmemArgs {
   int frames_per_cta;
   int W;          // staged window capacity per channel (samples, multiple of 4)
   int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
+  int jc;         // receive channels per staged chunk: 32 or 64
 };
 
 // ---- tcgen05 (TMEM) helpers
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
   const int W = a.W;
+  const int TJC = a.jc;
 
   // shared memory: [tmem base][tmin|tmax][meta ring][windows]
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -305,12 +307,12 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   };
   // cp.async staging: 4 threads per channel, 16 B copies at fixed slots
   // o = 4*(tid % 4) + 16*i, i < ceil(W / 16) <= 16
-  const int ld_jj = tid >> 2, ld_o = 4 * (tid & 3);
-  const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
+  const int ld_o = 4 * (tid & 3);  // channel jj = tid / 4 (+ 32 per sub-chunk)
   // returns the fast path's source pointer, which the caller keeps live
   // until the end of the iteration so that no instruction overwrites a
   // register an in-flight cp.async still reads (a write-after-read stall)
-  auto issue_loads = [&](int slot, int tslot, const Cursor& cu) -> const float* {
+  auto issue_loads = [&](int slot, int tslot, const Cursor& cu, int ld_jj) -> const float* {
+    const int64_t ld_trace = (int64_t)ld_jj * n_s + ld_o;
     const int j = cu.cb * TJC + ld_jj;
     if ((HYB && tid >= 128) || j >= n_rx) return nullptr;
     const int2 mm = make_int2(metaX[tslot * nrp + j], metaK[tslot * nrp + j]);
@@ -409,7 +411,9 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   if (n_T > 1) make_meta(1);
   __syncthreads();
   for (int p = 0; p < 2; ++p) {
-    if (p < Q) issue_loads(slot_ld, tslot_ld, nx2);
+    if (p < Q)
+      for (int sub = 0; sub < TJC / 32; ++sub)
+        issue_loads(slot_ld, tslot_ld, nx2, (tid >> 2) + 32 * sub);
     cp_async_commit();
     advance(nx2, slot_ld, tslot_ld);
   }
@@ -427,7 +431,11 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       if (n_chunks < 2) __syncthreads();  // first used by this iteration's loads
     }
     const float* keep = nullptr;
-    if (q + 2 < Q) keep = issue_loads(slot_ld, tslot_ld, nx2);
+    const float* keep2 = nullptr;
+    if (q + 2 < Q) {
+      keep = issue_loads(slot_ld, tslot_ld, nx2, tid >> 2);
+      if (TJC > 32) keep2 = issue_loads(slot_ld, tslot_ld, nx2, (tid >> 2) + 32);
+    }
     cp_async_commit();
     advance(nx2, slot_ld, tslot_ld);
     if (cur.cb == 0) {
@@ -480,7 +488,6 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       // identity map: channels cb*32 .. cb*32+31 are elements of the same
       // index -- tcgen05.ld.x32 fetches 16 delay pairs (PAIR) or 32 delays
       if (PAIR) {
-#pragma unroll
         for (int h = 0; h < TJC; h += 16) {
           u64 d[16];
           if (tm_warp) {
@@ -499,15 +506,17 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
           }
         }
       } else {
-        float d[32];
-        tm_ld32f(tlane + cur.cb * TJC, d);
+        for (int h = 0; h < TJC; h += 32) {
+          float d[32];
+          tm_ld32f(tlane + cur.cb * TJC + h, d);
 #pragma unroll
-        for (int i = 0; i < TJC; i += 4) {
-          const int4 k4 = MK4[i >> 2];
-          channel(L::make(d[i], 0.0f), (uint32_t)k4.x);
-          channel(L::make(d[i + 1], 0.0f), (uint32_t)k4.y);
-          channel(L::make(d[i + 2], 0.0f), (uint32_t)k4.z);
-          channel(L::make(d[i + 3], 0.0f), (uint32_t)k4.w);
+          for (int i = 0; i < 32; i += 4) {
+            const int4 k4 = MK4[(h + i) >> 2];
+            channel(L::make(d[i], 0.0f), (uint32_t)k4.x);
+            channel(L::make(d[i + 1], 0.0f), (uint32_t)k4.y);
+            channel(L::make(d[i + 2], 0.0f), (uint32_t)k4.z);
+            channel(L::make(d[i + 3], 0.0f), (uint32_t)k4.w);
+          }
         }
       }
     } else {
@@ -539,7 +548,7 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       acc = L::splat(0.0f);
     }
     advance(cur, slot_cur, tslot_cur);
-    asm volatile("" ::"l"(keep));
+    asm volatile("" ::"l"(keep), "l"(keep2));
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 
@@ -553,14 +562,14 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
 // variant of the TMEM kernel a launch uses
 enum TmemVariant { kScalar = 0, kPair = 1, kHybrid = 2 };
 
-static size_t tmem_smem_bytes(const bm_das_geometry& g, int W, int variant) {
+static size_t tmem_smem_bytes(const bm_das_geometry& g, int W, int variant, int jc = 32) {
   const int nth = variant == kHybrid ? 192 : 128;
   size_t b = 16 + (size_t)g.n_tx * 16;
   b = ((b + 15) & ~size_t(15)) + (size_t)g.n_elements * 8;
   b = ((b + 15) & ~size_t(15)) + (size_t)((g.n_rx + 3) & ~3) * 24;
   if (g.scheme == BM_PW && variant != kHybrid) b += (size_t)g.n_tx * nth * 8;
   if (variant == kHybrid) b += (size_t)g.n_elements * 64 * 8;
-  return b + (size_t)NST * TJC * W * 4;
+  return b + (size_t)NST * jc * W * 4;
 }
 
 static int tmem_cols_for(int n_el, bool pair) {
@@ -598,15 +607,18 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   const int variant = tmem_variant(g);
   const bool pair = variant != kScalar, hyb = variant == kHybrid;
   TmemArgs a{g, (const float*)rf, rf_stride, (float*)out, out_stride, n_frames, 1,
-             hyb ? g.window_hint_wide : g.window_hint, tmem_cols_for(g.n_elements, pair)};
+             hyb ? g.window_hint_wide : g.window_hint, tmem_cols_for(g.n_elements, pair), 32};
   const int tz = pair ? 16 : 8, tx = hyb ? 24 : TX, nth = hyb ? 192 : 128;
   const int tiles = ((g.n_z + tz - 1) / tz) * ((g.n_x + tx - 1) / tx);
   // CTAs per SM are limited to what TMEM holds (512 columns): request enough
   // shared memory that no extra CTA is scheduled to spin in tcgen05.alloc
   int per_sm = 512 / a.tmem_cols;
   if (per_sm > 4) per_sm = 4;
-  size_t smem = tmem_smem_bytes(g, a.W, variant);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
+  // 64-channel chunks halve the per-chunk overhead (cfg2: 5.87 vs 6.30 ms
+  // per 32 frames) when their windows still fit the SMEM share of a CTA
+  if (g.n_rx >= 64 && tmem_smem_bytes(g, a.W, variant, 64) <= cap) a.jc = 64;
+  size_t smem = tmem_smem_bytes(g, a.W, variant, a.jc);
   if (smem < cap) smem = cap;
   // frames per CTA: amortise the per-CTA delay-table build over a frame
   // group while keeping >= 4 waves of CTAs for load balance
