@@ -34,7 +34,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "cfg2 PWI 128el x 11 angles x 2048 samples -> 512x512, DAS+envelope+dB30, linear"
+WORKLOADS = {
+    "cfg1": "cfg1 STAI 64el x 64tx x 2048 samples -> 256x256, DAS+envelope+dB30, linear",
+    "cfg2": "cfg2 PWI 128el x 11 angles x 2048 samples -> 512x512, DAS+envelope+dB30, linear",
+    "cfg3": "cfg3 STAI 128el x 128tx x 4096 samples -> 1024x512, DAS+envelope+dB30, linear",
+}
+WORKLOAD = WORKLOADS["cfg2"]
 
 
 def parse():
@@ -200,6 +205,8 @@ def main():
     from paper_1811_01566_b200 import environment as ME
 
     ctx, grid, n_s = ME.config_geometry(args.config)
+    global WORKLOAD
+    WORKLOAD = WORKLOADS.get(args.config, WORKLOAD).replace("linear", args.interp)
     frame_bytes = ctx.n_tx * ctx.n_elements * n_s * 4
     img_bytes = grid.n_z * grid.n_x * 4
 
@@ -347,7 +354,8 @@ def main():
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-        "kernel": "bm_das_beamform (das_tmem_kernel)", "kernel_ms_per_launch": round(das_ms, 4),
+        "kernel": f"bm_das_beamform ({eng.plan.kernel_for(n_s, args.interp)})",
+        "kernel_ms_per_launch": round(das_ms, 4),
         "algorithmic_bytes_per_launch": das_bytes,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
         "note": "DAS is FP32-pipe bound, not HBM bound: see binding",

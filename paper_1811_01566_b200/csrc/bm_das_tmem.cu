@@ -140,7 +140,7 @@ __device__ __forceinline__ void tm_ld32f(uint32_t taddr, float (&d)[32]) {
 // HYB (pair only): a 6-warp CTA whose warps 4-5 keep their delay table in
 // SHARED memory next to the four TMEM warps -- TMEM caps the SM at 8 warps,
 // TMEM + SMEM together hold 12.  Tile 16 x 24 (warps 4-5: columns 16-23).
-template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP, bool HYB>
+template <bool PAIR, bool PW, bool LINEAR, bool T0, bool IDMAP, bool HYB, int TJC>
 __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel(const TmemArgs a) {
   using O = R<float>;
   using L = Lane<PAIR>;
@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx, n_s = g.n_samples;
   const int W = a.W;
-  const int TJC = a.jc;
 
   // shared memory: [tmem base][tmin|tmax][meta ring][windows]
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -488,6 +487,7 @@ __global__ void __launch_bounds__(HYB ? 192 : 128, PAIR ? 2 : 4) das_tmem_kernel
       // identity map: channels cb*32 .. cb*32+31 are elements of the same
       // index -- tcgen05.ld.x32 fetches 16 delay pairs (PAIR) or 32 delays
       if (PAIR) {
+#pragma unroll
         for (int h = 0; h < TJC; h += 16) {
           u64 d[16];
           if (tm_warp) {
@@ -617,7 +617,7 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   // 64-channel chunks halve the per-chunk overhead (cfg2: 5.87 vs 6.30 ms
   // per 32 frames) when their windows still fit the SMEM share of a CTA
-  if (g.n_rx >= 64 && tmem_smem_bytes(g, a.W, variant, 64) <= cap) a.jc = 64;
+  if (variant == kPair && g.n_rx >= 64 && tmem_smem_bytes(g, a.W, variant, 64) <= cap) a.jc = 64;
   size_t smem = tmem_smem_bytes(g, a.W, variant, a.jc);
   if (smem < cap) smem = cap;
   // frames per CTA: amortise the per-CTA delay-table build over a frame
@@ -629,27 +629,30 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
   a.frames_per_cta = fpc;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const TmemArgs);
-#define BM_TMEM_ROW(P, H)                                                                    \
-  das_tmem_kernel<P, false, false, false, false, H>,                                        \
-      das_tmem_kernel<P, false, false, false, true, H>,                                     \
-      das_tmem_kernel<P, false, false, true, false, H>,                                     \
-      das_tmem_kernel<P, false, false, true, true, H>,                                      \
-      das_tmem_kernel<P, false, true, false, false, H>,                                     \
-      das_tmem_kernel<P, false, true, false, true, H>,                                      \
-      das_tmem_kernel<P, false, true, true, false, H>,                                      \
-      das_tmem_kernel<P, false, true, true, true, H>,                                       \
-      das_tmem_kernel<P, true, false, false, false, H>,                                     \
-      das_tmem_kernel<P, true, false, false, true, H>,                                      \
-      das_tmem_kernel<P, true, false, true, false, H>,                                      \
-      das_tmem_kernel<P, true, false, true, true, H>,                                       \
-      das_tmem_kernel<P, true, true, false, false, H>,                                      \
-      das_tmem_kernel<P, true, true, false, true, H>,                                       \
-      das_tmem_kernel<P, true, true, true, false, H>, das_tmem_kernel<P, true, true, true, true, H>
-  static const kfn table[48] = {BM_TMEM_ROW(false, false), BM_TMEM_ROW(true, false),
-                                BM_TMEM_ROW(true, true)};
+#define BM_TMEM_ROW(P, H, J)                                                                 \
+  das_tmem_kernel<P, false, false, false, false, H, J>,                                     \
+      das_tmem_kernel<P, false, false, false, true, H, J>,                                  \
+      das_tmem_kernel<P, false, false, true, false, H, J>,                                  \
+      das_tmem_kernel<P, false, false, true, true, H, J>,                                   \
+      das_tmem_kernel<P, false, true, false, false, H, J>,                                  \
+      das_tmem_kernel<P, false, true, false, true, H, J>,                                   \
+      das_tmem_kernel<P, false, true, true, false, H, J>,                                   \
+      das_tmem_kernel<P, false, true, true, true, H, J>,                                    \
+      das_tmem_kernel<P, true, false, false, false, H, J>,                                  \
+      das_tmem_kernel<P, true, false, false, true, H, J>,                                   \
+      das_tmem_kernel<P, true, false, true, false, H, J>,                                   \
+      das_tmem_kernel<P, true, false, true, true, H, J>,                                    \
+      das_tmem_kernel<P, true, true, false, false, H, J>,                                   \
+      das_tmem_kernel<P, true, true, false, true, H, J>,                                    \
+      das_tmem_kernel<P, true, true, true, false, H, J>,                                    \
+      das_tmem_kernel<P, true, true, true, true, H, J>
+  // rows: scalar/32, pair/32, hybrid/32, pair/64
+  static const kfn table[64] = {BM_TMEM_ROW(false, false, 32), BM_TMEM_ROW(true, false, 32),
+                                BM_TMEM_ROW(true, true, 32), BM_TMEM_ROW(true, false, 64)};
 #undef BM_TMEM_ROW
-  const kfn k = table[16 * variant + ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
-                                      (g.rx_identity ? 1 : 0))];
+  const int row = (variant == kPair && a.jc == 64) ? 3 : variant;
+  const kfn k = table[16 * row + ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) |
+                                  (g.rx_identity ? 1 : 0))];
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);

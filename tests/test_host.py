@@ -138,9 +138,9 @@ def test_no_contracted_fma_in_das_kernels():
     the correctly-rounded sqrt/div sequences."""
     funcs = _sass_by_function()
     das = {n: l for n, l in funcs.items() if "das_fast_kernel" in n or "das_tmem_kernel" in n}
-    # (smem, tmem-scalar, tmem-pair, tmem-hybrid) x {STA, PW} x {nearest, linear}
-    # x {t0, no t0} x {identity map, general}
-    assert len(das) == 64
+    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch) x {STA, PW}
+    # x {nearest, linear} x {t0, no t0} x {identity map, general}
+    assert len(das) == 80
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
