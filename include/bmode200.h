@@ -77,7 +77,8 @@ typedef struct bm_das_geometry {
                           kernel then keeps the reference's "- t0" rounding step) */
   int32_t rx_identity; /* set by bm_das_prepare: 1 if rx_map[e][j] == j for all e, j */
   int32_t window_hint_wide; /* set by bm_das_prepare: window bound of 16 x 24 tiles */
-  int32_t reserved;
+  int32_t window_hint_g4; /* set by bm_das_prepare: window bound of a 16 x 16 tile
+                             over 4 adjacent elements (one TMA box; 0 = unusable) */
   double speed_of_sound;     /* c  (cast to dtype, beamform.py:206)          */
   double sampling_frequency; /* fs (cast to dtype, beamform.py:207)          */
   const double* elem_x;      /* [n_elements] element centres, f64            */

@@ -32,7 +32,7 @@ class DasGeometry(ctypes.Structure):
         ("n_elements", ctypes.c_int32), ("n_z", ctypes.c_int32), ("n_x", ctypes.c_int32),
         ("window_hint", ctypes.c_int32), ("t0_nonzero", ctypes.c_int32),
         ("rx_identity", ctypes.c_int32), ("window_hint_wide", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("window_hint_g4", ctypes.c_int32),
         ("speed_of_sound", ctypes.c_double), ("sampling_frequency", ctypes.c_double),
         ("elem_x", ctypes.c_void_p), ("x_pos", ctypes.c_void_p), ("z_pos", ctypes.c_void_p),
         ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),

@@ -168,7 +168,8 @@ class DasPlan:
         g.interp = N.BM_NEAREST if interp == "nearest" else N.BM_LINEAR
         return g
 
-    KERNELS = {0: "generic", 1: "smem", 2: "tmem-scalar", 3: "tmem-pair", 4: "tmem-hybrid"}
+    KERNELS = {0: "generic", 1: "smem", 2: "tmem-scalar", 3: "tmem-pair", 4: "tmem-hybrid",
+               5: "tma-ws"}
 
     def kernel_for(self, n_samples: int, interp: str = "linear", fast: bool = True) -> str:
         """Name of the CUDA kernel a launch with this trace length would use."""

@@ -56,7 +56,11 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
 int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                     int64_t out_stride, int n_frames, cudaStream_t s);
-int das_tmem_variant(const bm_das_geometry& g);  // 0 scalar, 1 pair, 2 hybrid
+int das_tmem_variant(const bm_das_geometry& g);
+int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride);
+// returns -1 when this launch cannot use the TMA kernel (caller falls back)
+int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                   int64_t out_stride, int n_frames, cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid
 
 // DAS kernel selection: BM_DAS_KERNEL = auto (default) | tmem | smem | generic
 inline int das_kernel_choice() {
@@ -67,6 +71,7 @@ inline int das_kernel_choice() {
     if (e && !strcmp(e, "tmem")) choice = 1;
     if (e && !strcmp(e, "smem")) choice = 2;
     if (e && !strcmp(e, "generic")) choice = 3;
+    if (e && !strcmp(e, "tma")) choice = 4;
   }
   return choice;
 }

@@ -236,6 +236,7 @@ extern "C" int bm_das_aperture_span(const bm_das_geometry* g, double f_number,
 extern "C" int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride) {
   if (bm::check_geometry(g)) return -1;
   const int choice = bm::das_kernel_choice();
+  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride)) return 5;
   if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
     return 2 + bm::das_tmem_variant(*g);
   if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride)) return 1;
@@ -251,6 +252,10 @@ extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t
   if (n_frames == 0) return BM_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int choice = bm::das_kernel_choice();
+  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride)) {
+    rc = bm::das_tma_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
+    if (rc >= 0) return rc;  // -1: unaligned RF pointer etc. -> next kernel
+  }
   if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
     return bm::das_tmem_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
   if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride))

@@ -364,6 +364,7 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   if (!g || !elem_x || !x || !z || !t0_smp || !rx_map) return BM_ERR_INVALID_ARGUMENT;
   g->window_hint = 0;
   g->window_hint_wide = 0;
+  g->window_hint_g4 = 0;
   g->t0_nonzero = 1;
   g->rx_identity = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
@@ -412,5 +413,14 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   if (W_wide > 4096) return BM_OK;
   g->window_hint = W;
   g->window_hint_wide = W_wide;
+  // 4 adjacent elements share one window: rx delays are k-Lipschitz in the
+  // element position, so the union spans at most W + k * (x[m+3] - x[m]);
+  // rounded to 8 samples (128-B aligned 4-row TMA boxes)
+  if (g->n_elements >= 4) {
+    double ext = 0.0;
+    for (int m = 0; m + 3 < g->n_elements; ++m) ext = fmax(ext, fabs(elem_x[m + 3] - elem_x[m]));
+    const int wg = (int)ceil(W + k * ext + 4.0);
+    g->window_hint_g4 = (wg + 7) & ~7;
+  }
   return BM_OK;
 }

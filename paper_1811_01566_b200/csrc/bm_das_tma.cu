@@ -1,0 +1,471 @@
+// K1, warp-specialised: TMA-fed RF windows, receive delays in TENSOR MEMORY.
+//
+// Same arithmetic -- and therefore the same bits -- as das_tmem_kernel and
+// the reference's f32 das_beamform (beamform.py:122-187 with the DasPlan
+// delays of :211-228).  What changes is who moves the data:
+//
+//  * das_tmem_kernel: every warp computes staging metadata, issues its share
+//    of the cp.async window copies and meets the others at one __syncthreads
+//    per chunk.  ncu (profiles/r01_das_tmem_ncu.txt) puts ~35 % of the warp
+//    samples of that kernel outside the gather/interpolate loop.
+//  * here a fifth PRODUCER warp owns all of it: per chunk of TJC receive
+//    channels it computes each channel's window start, publishes the gather
+//    base K, and issues one cp.async.bulk.tensor (TMA) per channel window
+//    [ws, ws + W) of trace (frame, e, j).  TMA's out-of-bounds fill writes
+//    exact zeros for samples outside [0, n_s) -- the reference's sentinel
+//    semantics (beamform.py:127-137) without a slow path.  The four CONSUMER
+//    warps only wait on the stage's full barrier, gather and interpolate, and
+//    release the stage through its empty barrier: no CTA-wide barrier in the
+//    loop.
+//
+// Tile and lane layout are das_tmem_kernel's PAIR layout: 16 x 16 pixels per
+// CTA, thread (warp w < 4, lane l) owns pixels (row l/8, col l%8) and
+// (row l/8 + 4, col l%8) of its warp's 8 x 8 block, TMEM lane 32w + l holds
+// the pair's delays to element m in columns 2m, 2m+1.
+#include <cuda.h>  // CUtensorMap
+
+#include "bm_tmem.cuh"
+
+namespace bm {
+
+constexpr int kTmaMaxStages = 8;
+
+struct TmaArgs {
+  bm_das_geometry g;
+  float* out;
+  int64_t out_stride;
+  int n_frames;
+  int frames_per_cta;
+  int W;          // samples per channel window (multiple of 32: 128-B aligned rows)
+  int nst;        // pipeline stages (2 .. kTmaMaxStages)
+  int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
+};
+
+// shared-memory carve (bytes), identical on host and device
+struct TmaLayout {
+  int tmin, rmin, metaK, metaM, txd, win, total;
+  __host__ __device__ TmaLayout(int n_tx, int n_el, int tjc, int nst, int W, bool pw) {
+    tmin = 256;  // [0,16) TMEM base, [64,128) full barriers, [128,192) empty barriers
+    rmin = (tmin + 16 * n_tx + 15) & ~15;
+    metaK = (rmin + 8 * n_el + 15) & ~15;
+    metaM = metaK + 4 * tjc * nst;
+    txd = metaM + 4 * tjc * nst;
+    win = (txd + (pw ? n_tx * 128 * 8 : 0) + 127) & ~127;
+    total = win + nst * tjc * W * 4;
+  }
+};
+
+// ---- mbarrier / TMA helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "BM_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra BM_WAIT;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC>
+__global__ void __launch_bounds__(160, 2)
+    das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
+  using O = R<float>;
+  using L = Lane<true>;
+  typedef u64 VT;
+  constexpr int NTH = 160, NC = 128;  // threads, consumer threads
+  constexpr int TZk = 16, TXk = 16;
+  constexpr int G = IDMAP ? 4 : 1;  // receive channels per TMA box (rows of W samples)
+  const bm_das_geometry& g = a.g;
+  const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx;
+  const int W = a.W, nst = a.nst;
+  const TmaLayout lay(n_tx, n_el, TJC, nst, W, PW);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
+  const uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t full_s = smem_s + 64, empty_s = smem_s + 128;  // + 8 * stage
+  float* tmin = reinterpret_cast<float*>(smem_raw + lay.tmin);  // [n_tx]
+  float* tmax = tmin + n_tx;                                    // [n_tx]
+  float* t0v = tmax + n_tx;                                     // [n_tx] fs*t0
+  int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
+  float* rmin = reinterpret_cast<float*>(smem_raw + lay.rmin);  // [n_el]
+  float* rmax = rmin + n_el;                                    // [n_el]
+  int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][TJC] gather base K
+  int* metaM = reinterpret_cast<int*>(smem_raw + lay.metaM);    // [nst][TJC] element m
+  u64* txd_s = reinterpret_cast<u64*>(smem_raw + lay.txd);      // PW: [n_tx][128]
+  const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC][W] f32
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp == 4;
+  const int tiles_x = (g.n_x + TXk - 1) / TXk;
+  const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TXk;
+  const int col = tx0 + (warp & 1) * 8 + (lane & 7);
+  const int rowA = tz0 + ((warp >> 1) & 1) * 8 + (lane >> 3), rowB = rowA + 4;
+  const int colc = min(col, g.n_x - 1);
+  const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
+
+  const float c = O::from_double(g.speed_of_sound);
+  const float fs = O::from_double(g.sampling_frequency);
+  const double px = g.x_pos[colc];
+  const float pxd = O::from_double(px);
+  const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
+
+  // ---- TMEM allocation (warp 0), barrier init (producer lane 0)
+  if (warp == 0) {
+    tm_alloc(smem_s, (uint32_t)a.tmem_cols);
+    tm_relinquish();
+  }
+  if (producer && lane == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(full_s + 8 * s, 32);  // the producer's 32 lanes (one carries expect_tx)
+      mbar_init(empty_s + 8 * s, 4);  // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rf_map)) : "memory");
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
+
+  // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
+  if (!producer) {
+    for (int m = 0; m < n_el; ++m) {
+      const float dx = O::from_double(g.elem_x[m] - px);
+      const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
+      const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
+      tm_st2(tlane + 2 * m, dA, dB);
+    }
+    tm_wait_st();
+  }
+
+  const int zl = min(tz0 + TZk, g.n_z) - 1;
+  const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TXk, g.n_x) - 1];
+  const double z0 = g.z_pos[tz0], z1 = g.z_pos[zl];
+  const double k = g.sampling_frequency / g.speed_of_sound;
+  // receive-path delay bounds of element m over the tile rectangle (samples);
+  // float arithmetic: the window margins of 3-4 samples absorb its error
+  const float kf = (float)k, x0f = (float)x0, x1f = (float)x1, z0f = (float)z0, z1f = (float)z1;
+  auto rx_bounds = [&](int m, float& lo, float& hi) {
+    const float xm = (float)g.elem_x[m];
+    const float dmin = fmaxf(0.0f, fmaxf(x0f - xm, xm - x1f));
+    const float dmax = fmaxf(fabsf(x0f - xm), fabsf(x1f - xm));
+    lo = kf * sqrtf(dmin * dmin + z0f * z0f);
+    hi = kf * sqrtf(dmax * dmax + z1f * z1f);
+  };
+  for (int m = tid; m < n_el; m += NTH) rx_bounds(m, rmin[m], rmax[m]);
+  for (int e = tid; e < n_tx; e += NTH) {
+    t0v[e] = reinterpret_cast<const float*>(g.t0_smp)[e];
+    if (!PW) txe[e] = g.tx_elements[e];
+    if (PW) {
+      const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
+      const double sa = reinterpret_cast<const float*>(g.sin_a)[e];
+      const double v00 = z0 * ca + x0 * sa, v01 = z0 * ca + x1 * sa;
+      const double v10 = z1 * ca + x0 * sa, v11 = z1 * ca + x1 * sa;
+      tmin[e] = (float)(k * fmin(fmin(v00, v01), fmin(v10, v11)));
+      tmax[e] = (float)(k * fmax(fmax(v00, v01), fmax(v10, v11)));
+    } else {
+      rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
+    }
+  }
+  if (PW && !producer) {
+    // exact transmit delays fs*((z cos + x sin)/c) of the pixel pair for every
+    // angle (beamform.py:218-225), once per CTA
+    for (int e = 0; e < n_tx; ++e) {
+      const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
+      const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+      const float xs = O::mul(pxd, sa);
+      const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+      const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
+      txd_s[e * NC + tid] = pk(tA, tB);
+    }
+  }
+  __syncthreads();
+
+  const int n_chunks = (n_rx + TJC - 1) / TJC;
+  const int f_begin = blockIdx.y * a.frames_per_cta;
+  const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
+  const int Q = f_count * n_tx * n_chunks;
+
+  if (producer) {
+    // ================= producer warp: window starts + TMA issue
+    Cursor cu{0, 0, 0, 0};
+    int s = 0, r = 0;  // stage, round (q = r * nst + s)
+    for (int q = 0; q < Q; ++q) {
+      // round r >= 1 reuses stage s: wait for the consumers' release of round r-1
+      if (r > 0) mbar_wait(empty_s + 8 * s, (uint32_t)(r - 1) & 1u);
+      const int e = cu.e;
+      const float t0 = t0v[e];
+      const float lo_e = tmin[e] - t0;
+      const int jb = cu.cb * TJC;
+      const int jn = min(TJC, n_rx - jb);
+      const int row0 = e * n_rx + jb;
+      const int fr = f_begin + cu.fl;
+      const uint32_t bar = full_s + 8 * s;
+      const int ngr = (jn + G - 1) / G;  // boxes this chunk
+#pragma unroll
+      for (int u = 0; u < (TJC / G + 31) / 32; ++u) {
+        const int gi = lane + 32 * u;
+        if (gi < ngr) {
+          const int jj0 = gi * G;
+          int m = jb + jj0;
+          float rlo = rmin[m];
+          if (IDMAP) {  // G adjacent elements share the window
+#pragma unroll
+            for (int i = 1; i < G; ++i)
+              if (jj0 + i < jn) rlo = fminf(rlo, rmin[m + i]);
+          } else {
+            m = g.rx_map[(int64_t)e * n_rx + jb + jj0];
+            rlo = rmin[m];
+            metaM[s * TJC + jj0] = m;
+          }
+          const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
+          const uint32_t dst = win_s + (uint32_t)((s * TJC + jj0) * W) * 4u;
+          const uint32_t K0 = dst - (uint32_t)(kMagicBits + ws) * 4u;
+          if (G == 4) {
+            const uint32_t rs = (uint32_t)W * 4u;
+            *reinterpret_cast<int4*>(metaK + s * TJC + jj0) =
+                make_int4((int)K0, (int)(K0 + rs), (int)(K0 + 2 * rs), (int)(K0 + 3 * rs));
+          } else {
+            metaK[s * TJC + jj0] = (int)K0;
+          }
+          tma_load_3d(dst, &rf_map, ws, row0 + jj0, fr, bar);
+        }
+      }
+      if (lane == 0)
+        mbar_arrive_tx(bar, (uint32_t)(ngr * G * W * 4));
+      else
+        mbar_arrive(bar);
+      cu.next(n_chunks, n_tx);
+      if (++s == nst) {
+        s = 0;
+        ++r;
+      }
+    }
+  } else {
+    // ================= consumer warps: gather + interpolate + accumulate
+    const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
+    const VT ONE2 = L::splat(1.0f), HALF2 = L::splat(0.5f);
+    VT acc = L::splat(0.0f);  // +0.0f
+    VT txd = acc, t0e2 = acc;
+    Cursor cur{0, 0, 0, 0};
+    int s = 0;
+    uint32_t ph = 0;
+    for (int q = 0; q < Q; ++q) {
+      mbar_wait(full_s + 8 * s, ph);
+      if (cur.cb == 0) {
+        if (PW)
+          txd = (VT)txd_s[cur.e * NC + tid];
+        else
+          txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
+        t0e2 = L::splat(t0v[cur.e]);
+      }
+      const int* MKc = metaK + s * TJC;
+      const int* MMc = metaM + s * TJC;
+      const int4* MK4 = reinterpret_cast<const int4*>(MKc);  // 4 gather bases per LDS.128
+      const int jn = min(TJC, n_rx - cur.cb * TJC);
+
+      // one channel: rxd = receive delays of the pair, K = gather address base
+      auto channel = [&](VT rxd, uint32_t K) {
+        VT t = L::add(txd, rxd);
+        if (T0) t = L::sub(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
+        const VT r = LINEAR ? L::add_rm(t, M2) : L::add_rm(L::add(t, HALF2), M2);
+        float rA, rB;
+        unpk((u64)r, rA, rB);
+        const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
+        const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
+        if (LINEAR) {
+          const VT x0 = L::make(lds0(aA), lds0(aB));
+          const VT x1 = L::make(lds1(aA), lds1(aB));
+          const VT fr = L::sub(t, L::add(r, NM2));  // a = t - floor(t)
+          const VT om = L::sub(ONE2, fr);           // 1 - a
+          acc = L::add(acc, L::mul(om, x0));        // acc = out + (1 - a) * x[k0]
+          acc = L::add(acc, L::mul(fr, x1));        // out = acc + a * x[k1]
+        } else {
+          acc = L::add(acc, L::make(lds0(aA), lds0(aB)));
+        }
+      };
+      if (IDMAP && jn == TJC) {
+        // identity map: channel j is element j -- one tcgen05.ld.x32 fetches
+        // the delay pairs of 16 consecutive channels
+#pragma unroll
+        for (int h = 0; h < TJC; h += 16) {
+          u64 d[16];
+          tm_ld32(tlane + 2 * (cur.cb * TJC + h), d);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const int4 k4 = MK4[(h + i) >> 2];
+            channel((VT)d[i], (uint32_t)k4.x);
+            channel((VT)d[i + 1], (uint32_t)k4.y);
+            channel((VT)d[i + 2], (uint32_t)k4.z);
+            channel((VT)d[i + 3], (uint32_t)k4.w);
+          }
+        }
+      } else {
+        for (int jj = 0; jj < jn; ++jj) {
+          const int m = IDMAP ? cur.cb * TJC + jj : MMc[jj];
+          channel((VT)tm_ld2(tlane + 2 * m), (uint32_t)MKc[jj]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_s + 8 * s);  // stage s may be refilled
+
+      if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
+        const int64_t fo = (int64_t)(f_begin + cur.fl) * a.out_stride;
+        if (col < g.n_x) {
+          float oA, oB;
+          unpk((u64)acc, oA, oB);
+          if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
+          if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = oB;
+        }
+        acc = L::splat(0.0f);
+      }
+      cur.next(n_chunks, n_tx);
+      if (++s == nst) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  }
+
+  // ---- release TMEM (the allocating warp)
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  if (warp == 0) tm_dealloc(tbase, (uint32_t)a.tmem_cols);
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// row stride of the staged windows: one channel per box (128-B aligned rows)
+// or 4 adjacent channels per box sharing one window start
+static int tma_window(const bm_das_geometry& g) {
+  return g.rx_identity && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
+}
+
+// channels per stage and stage count for the shared-memory share of one CTA
+static bool tma_plan(const bm_das_geometry& g, int& tjc, int& nst, size_t& smem) {
+  const int W = tma_window(g);
+  const int per_sm = 2 * g.n_elements <= 256 ? 2 : 1;
+  const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
+  const bool pw = g.scheme == BM_PW;
+  for (int t : {64, 32}) {
+    if (t == 64 && g.n_rx < 64) continue;
+    int n = kTmaMaxStages;
+    while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw).total > cap) --n;
+    if (n >= (t == 64 ? 3 : 2)) {
+      tjc = t;
+      nst = n;
+      smem = cap;
+      return true;
+    }
+  }
+  return false;
+}
+
+int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
+  if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0 || tma_window(g) > 256) return 0;
+  if (g.rx_identity && g.window_hint_g4 <= 0) return 0;  // 4-channel boxes need the bound
+  if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;  // 16-B TMA strides
+  if (2 * g.n_elements > 512) return 0;                       // pair layout in TMEM
+  if ((int64_t)g.n_tx * g.n_rx > 0x7fffffffLL) return 0;
+  int tjc, nst;
+  size_t smem;
+  if (!tma_plan(g, tjc, nst, smem)) return 0;
+  return encode_tiled() != nullptr;
+}
+
+int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                   int64_t out_stride, int n_frames, cudaStream_t s) {
+  if (((uintptr_t)rf & 15) != 0) return -1;  // caller falls back
+  int tjc, nst;
+  size_t smem;
+  if (!tma_plan(g, tjc, nst, smem)) return -1;
+  const int W = tma_window(g);
+  // RF as a 3-D tensor: samples x (transmit, channel) rows x frames
+  CUtensorMap map;
+  const int64_t fstride = n_frames > 1 ? rf_stride : (int64_t)g.n_tx * g.n_rx * g.n_samples;
+  cuuint64_t dims[3] = {(cuuint64_t)g.n_samples, (cuuint64_t)g.n_tx * g.n_rx,
+                        (cuuint64_t)n_frames};
+  cuuint64_t strides[2] = {(cuuint64_t)g.n_samples * 4, (cuuint64_t)fstride * 4};
+  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(rf), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
+  const int per_sm = 2 * g.n_elements <= 256 ? 2 : 1;
+  TmaArgs a{g, (float*)out, out_stride, n_frames, 1, W, nst, 2 * g.n_elements <= 256 ? 256 : 512};
+  int fpc = 1;
+  while (fpc < 16 && fpc * 2 <= n_frames &&
+         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
+    fpc *= 2;
+  a.frames_per_cta = fpc;
+  const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
+  typedef void (*kfn)(const CUtensorMap, const TmaArgs);
+#define BM_TMA_ROW(J)                                                                         \
+  das_tma_kernel<false, false, false, false, J>, das_tma_kernel<false, false, false, true, J>, \
+      das_tma_kernel<false, false, true, false, J>, das_tma_kernel<false, false, true, true, J>, \
+      das_tma_kernel<false, true, false, false, J>, das_tma_kernel<false, true, false, true, J>, \
+      das_tma_kernel<false, true, true, false, J>, das_tma_kernel<false, true, true, true, J>,   \
+      das_tma_kernel<true, false, false, false, J>, das_tma_kernel<true, false, false, true, J>, \
+      das_tma_kernel<true, false, true, false, J>, das_tma_kernel<true, false, true, true, J>,   \
+      das_tma_kernel<true, true, false, false, J>, das_tma_kernel<true, true, false, true, J>,   \
+      das_tma_kernel<true, true, true, false, J>, das_tma_kernel<true, true, true, true, J>
+  static const kfn table[32] = {BM_TMA_ROW(32), BM_TMA_ROW(64)};
+#undef BM_TMA_ROW
+  const kfn k = table[(tjc == 64 ? 16 : 0) + ((pw ? 8 : 0) | (lin ? 4 : 0) |
+                                             (g.t0_nonzero ? 2 : 0) | (g.rx_identity ? 1 : 0))];
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return BM_ERR_CUDA;
+  dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
+  k<<<grid, 160, smem, s>>>(map, a);
+  return cuda_status();
+}
+
+}  // namespace bm

@@ -1,0 +1,103 @@
+// tcgen05 tensor-memory helpers and the packed/scalar lane arithmetic shared
+// by the TMEM-resident DAS kernels (bm_das_tmem.cu, bm_das_tma.cu).
+#pragma once
+#include "bm_f32x2.cuh"
+
+namespace bm {
+
+// ---- tcgen05 (TMEM) helpers
+__device__ __forceinline__ void tm_alloc(uint32_t smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tm_relinquish() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tm_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, float a, float b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "f"(a), "f"(b)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// x2 load + wait; the wait takes the destinations as in-out operands so no
+// use of them can be scheduled before the load has landed.
+__device__ __forceinline__ u64 tm_ld2(uint32_t taddr) {
+  uint32_t a, b;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
+  return ((u64)b << 32) | a;
+}
+// 16 channel pairs (32 columns) in one instruction
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, u64 (&d)[16]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])::"memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d[i] = ((u64)r[2 * i + 1] << 32) | r[2 * i];
+}
+
+// Lane arithmetic: a thread owns PAIR ? two pixels (packed f32x2) : one pixel.
+template <bool PAIR> struct Lane;
+template <> struct Lane<true> {
+  typedef u64 T;
+  static __device__ __forceinline__ T splat(float a) { return pk(a, a); }
+  static __device__ __forceinline__ T make(float a, float b) { return pk(a, b); }
+  static __device__ __forceinline__ T add(T a, T b) { return add2(a, b); }
+  static __device__ __forceinline__ T add_rm(T a, T b) { return add2_rm(a, b); }
+  static __device__ __forceinline__ T sub(T a, T b) { return sub2(a, b); }
+  static __device__ __forceinline__ T mul(T a, T b) { return mul2(a, b); }
+};
+template <> struct Lane<false> {
+  typedef float T;
+  static __device__ __forceinline__ T splat(float a) { return a; }
+  static __device__ __forceinline__ T make(float a, float) { return a; }
+  static __device__ __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ T add_rm(T a, T b) { return __fadd_rd(a, b); }
+  static __device__ __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ T mul(T a, T b) { return __fmul_rn(a, b); }
+};
+
+__device__ __forceinline__ void tm_st1(uint32_t taddr, float a) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "f"(a) : "memory");
+}
+__device__ __forceinline__ float tm_ld1(uint32_t taddr) {
+  uint32_t a;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(a) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a)::"memory");
+  return __uint_as_float(a);
+}
+__device__ __forceinline__ void tm_ld32f(uint32_t taddr, float (&d)[32]) {
+  u64 p[16];
+  tm_ld32(taddr, p);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) unpk(p[i], d[2 * i], d[2 * i + 1]);
+}
+
+}  // namespace bm

@@ -137,10 +137,11 @@ def test_no_contracted_fma_in_das_kernels():
     with a zero addend (a plain rounded product) and scalar FFMA only inside
     the correctly-rounded sqrt/div sequences."""
     funcs = _sass_by_function()
-    das = {n: l for n, l in funcs.items() if "das_fast_kernel" in n or "das_tmem_kernel" in n}
-    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch) x {STA, PW}
-    # x {nearest, linear} x {t0, no t0} x {identity map, general}
-    assert len(das) == 80
+    das = {n: l for n, l in funcs.items()
+           if any(k in n for k in ("das_fast_kernel", "das_tmem_kernel", "das_tma_kernel"))}
+    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch, tma-32ch,
+    # tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0} x {identity map, general}
+    assert len(das) == 112
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
@@ -149,6 +150,10 @@ def test_no_contracted_fma_in_das_kernels():
         # the pair kernels, scalar for the one-pixel-per-thread TMEM kernel
         packed = not n.startswith("_ZN2bm15das_tmem_kernelILb0")
         assert any(("FADD2.RM" if packed else "FADD.RM") in l for l in lines), n
-        assert any("LDGSTS" in l for l in lines), n    # cp.async staging
-        if "das_tmem_kernel" in n:  # receive-delay table in tensor memory
+        if "das_tma_kernel" in n:  # TMA window staging, mbarrier pipeline
+            assert any("UTMALDG" in l for l in lines), n
+            assert any("SYNCS" in l for l in lines), n
+        else:
+            assert any("LDGSTS" in l for l in lines), n    # cp.async staging
+        if "das_tmem_kernel" in n or "das_tma_kernel" in n:  # delay table in tensor memory
             assert any("LDTM" in l for l in lines) and any("STTM" in l for l in lines), n
