@@ -147,6 +147,7 @@ class DasPlan:
         N.call("bm_das_prepare", ctypes.byref(g), he.ctypes.data, hx.ctypes.data,
                hz.ctypes.data, ht.ctypes.data, rx_map.ctypes.data)
         self.fast_window = int(g.window_hint)
+        self.tma_window = int(g.window_hint_g4)  # 4-channel TMA box width (samples)
         self._geom = g
         self.ctx, self.grid, self.apod, self.dtype, self.n_rx = ctx, grid, apod, dtype, n_rx
         self.device = dev

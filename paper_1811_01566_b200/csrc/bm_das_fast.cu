@@ -26,6 +26,10 @@
 //  * floor(t) and the integer sample index come from one FADD2.RM with the
 //    1.5*2^23 magic constant (exact for |t| < 2^22, checked on the host by
 //    bm_das_prepare); the index is the float's bit pattern, so no F2I.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "bm_f32x2.cuh"
 
 namespace bm {
@@ -358,6 +362,87 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
 
 }  // namespace bm
 
+// Host-only: the largest window a 16 x 16 tile needs for 4 adjacent elements,
+// evaluated per tile with the device's own bound arithmetic (das_tma_kernel:
+// tmin/tmax of the transmit path, rmin/rmax of each element):
+//   need <= max_e (tmax_e - tmin_e) + max_group (max rmax - min rmin) + 12
+// where 12 covers the -3 / align-to-4 / +4 window margins and the float
+// rounding of the device's sums and floors.  Returns 0 if the transmit
+// geometry cannot be read back.
+static int g4_window_bound(const bm_das_geometry* g, const double* elem_x, const double* x,
+                           const double* z) {
+  const int n_el = g->n_elements, n_tx = g->n_tx;
+  std::vector<float> ca(n_tx), sa(n_tx);
+  std::vector<int> te(n_tx);
+  const bool pw = g->scheme == BM_PW;
+  if (pw) {
+    const size_t es = g->dtype == BM_F64 ? 8 : 4;
+    std::vector<unsigned char> bc(es * n_tx), bs(es * n_tx);
+    if (!g->cos_a || !g->sin_a ||
+        cudaMemcpy(bc.data(), g->cos_a, es * n_tx, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(bs.data(), g->sin_a, es * n_tx, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    for (int e = 0; e < n_tx; ++e) {
+      ca[e] = es == 8 ? (float)reinterpret_cast<double*>(bc.data())[e]
+                      : reinterpret_cast<float*>(bc.data())[e];
+      sa[e] = es == 8 ? (float)reinterpret_cast<double*>(bs.data())[e]
+                      : reinterpret_cast<float*>(bs.data())[e];
+    }
+  } else {
+    if (!g->tx_elements ||
+        cudaMemcpy(te.data(), g->tx_elements, sizeof(int) * n_tx, cudaMemcpyDeviceToHost) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+  }
+  const double k = g->sampling_frequency / g->speed_of_sound;
+  const float kf = (float)k;
+  std::vector<float> rmin(n_el), rmax(n_el);
+  double need = 0.0;
+  for (int tz0 = 0; tz0 < g->n_z; tz0 += 16)
+    for (int tx0 = 0; tx0 < g->n_x; tx0 += 16) {
+      const double x0 = x[tx0], x1 = x[std::min(tx0 + 16, g->n_x) - 1];
+      const double z0 = z[tz0], z1 = z[std::min(tz0 + 16, g->n_z) - 1];
+      const float x0f = (float)x0, x1f = (float)x1, z0f = (float)z0, z1f = (float)z1;
+      for (int m = 0; m < n_el; ++m) {
+        const float xm = (float)elem_x[m];
+        const float dmin = std::max(0.0f, std::max(x0f - xm, xm - x1f));
+        const float dmax = std::max(std::fabs(x0f - xm), std::fabs(x1f - xm));
+        rmin[m] = kf * std::sqrt(dmin * dmin + z0f * z0f);
+        rmax[m] = kf * std::sqrt(dmax * dmax + z1f * z1f);
+      }
+      double txr = 0.0;
+      for (int e = 0; e < n_tx; ++e) {
+        if (pw) {
+          const double c = ca[e], s = sa[e];
+          const double v00 = z0 * c + x0 * s, v01 = z0 * c + x1 * s;
+          const double v10 = z1 * c + x0 * s, v11 = z1 * c + x1 * s;
+          const float lo = (float)(k * std::min(std::min(v00, v01), std::min(v10, v11)));
+          const float hi = (float)(k * std::max(std::max(v00, v01), std::max(v10, v11)));
+          txr = std::max(txr, (double)hi - (double)lo);
+        } else {
+          const int m = te[e];
+          if (m >= 0 && m < n_el) txr = std::max(txr, (double)rmax[m] - (double)rmin[m]);
+        }
+      }
+      double grp = 0.0;
+      for (int m0 = 0; m0 < n_el; m0 += 4) {
+        float lo = rmin[m0], hi = rmax[m0];
+        for (int m = m0 + 1; m < std::min(m0 + 4, n_el); ++m) {
+          lo = std::min(lo, rmin[m]);
+          hi = std::max(hi, rmax[m]);
+        }
+        grp = std::max(grp, (double)hi - (double)lo);
+      }
+      need = std::max(need, txr + grp);
+    }
+  const int w = (int)std::ceil(need) + 12;
+  return (w + 7) & ~7;
+}
+
 // Host-only: bound the fast kernel's per-(e, j) sample window over all tiles.
 extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const double* x,
                               const double* z, const double* t0_smp, const int32_t* rx_map) {
@@ -421,6 +506,8 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
     for (int m = 0; m + 3 < g->n_elements; ++m) ext = fmax(ext, fabs(elem_x[m + 3] - elem_x[m]));
     const int wg = (int)ceil(W + k * ext + 4.0);
     g->window_hint_g4 = (wg + 7) & ~7;
+    const int exact = g4_window_bound(g, elem_x, x, z);  // tighter where it can be read
+    if (exact > 0 && exact < g->window_hint_g4) g->window_hint_g4 = exact;
   }
   return BM_OK;
 }
