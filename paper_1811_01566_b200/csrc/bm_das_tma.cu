@@ -96,7 +96,11 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC>
+// WT: non-uniform receive apodisation (Hann and/or F-number gate): the
+// per-pixel weights w[m] live in TMEM next to the delays (columns
+// 2*n_el + 2m, 2m+1), and a contribution is acc + (w*(1-a))*x0 + (w*a)*x1
+// exactly as beamform.py:175-187 rounds it.
+template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false>
 __global__ void __launch_bounds__(160, 2)
     das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
   using O = R<float>;
@@ -167,6 +171,30 @@ __global__ void __launch_bounds__(160, 2)
       const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
       const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
       tm_st2(tlane + 2 * m, dA, dB);
+    }
+    if (WT) {
+      // receive apodisation (beamform.py:84-109): weight of element m is
+      // window[m - i0] inside the pixel's active span [i0, i1], 0 outside
+      int i0A = 0, i1A = n_el - 1, i0B = 0, i1B = n_el - 1;
+      if (g.span) {
+        const int64_t pA = (int64_t)rAc * g.n_x + colc, pB = (int64_t)rBc * g.n_x + colc;
+        i0A = g.span[2 * pA];
+        i1A = g.span[2 * pA + 1];
+        i0B = g.span[2 * pB];
+        i1B = g.span[2 * pB + 1];
+      }
+      auto row = [&](int i0, int i1) -> const float* {
+        if (g.window != BM_HANN) return nullptr;
+        const int cnt = max(0, min(i1 - i0 + 1, n_el));
+        return reinterpret_cast<const float*>(g.hann) + (int64_t)cnt * n_el;
+      };
+      const float* hA = row(i0A, i1A);
+      const float* hB = row(i0B, i1B);
+      for (int m = 0; m < n_el; ++m) {
+        const float wA = (m >= i0A && m <= i1A) ? (hA ? hA[m - i0A] : 1.0f) : 0.0f;
+        const float wB = (m >= i0B && m <= i1B) ? (hB ? hB[m - i0B] : 1.0f) : 0.0f;
+        tm_st2(tlane + 2 * n_el + 2 * m, wA, wB);
+      }
     }
     tm_wait_st();
   }
@@ -298,7 +326,7 @@ __global__ void __launch_bounds__(160, 2)
       const int jn = min(TJC, n_rx - cur.cb * TJC);
 
       // one channel: rxd = receive delays of the pair, K = gather address base
-      auto channel = [&](VT rxd, uint32_t K) {
+      auto channel = [&](VT rxd, VT wgt, uint32_t K) {
         VT t = L::add(txd, rxd);
         if (T0) t = L::sub(t, t0e2);  // all-zero t0 skips it: x - 0 == x exactly
         const VT r = LINEAR ? L::add_rm(t, M2) : L::add_rm(L::add(t, HALF2), M2);
@@ -311,37 +339,51 @@ __global__ void __launch_bounds__(160, 2)
           const VT x1 = L::make(lds1(aA), lds1(aB));
           const VT fr = L::sub(t, L::add(r, NM2));  // a = t - floor(t)
           const VT om = L::sub(ONE2, fr);           // 1 - a
-          acc = L::add(acc, L::mul(om, x0));        // acc = out + (1 - a) * x[k0]
-          acc = L::add(acc, L::mul(fr, x1));        // out = acc + a * x[k1]
+          if (WT) {
+            acc = L::add(acc, L::mul(L::mul(wgt, om), x0));  // out + (w*(1-a)) * x[k0]
+            acc = L::add(acc, L::mul(L::mul(wgt, fr), x1));  // acc + (w*a) * x[k1]
+          } else {
+            acc = L::add(acc, L::mul(om, x0));  // acc = out + (1 - a) * x[k0]
+            acc = L::add(acc, L::mul(fr, x1));  // out = acc + a * x[k1]
+          }
         } else {
-          acc = L::add(acc, L::make(lds0(aA), lds0(aB)));
+          const VT x = L::make(lds0(aA), lds0(aB));
+          acc = L::add(acc, WT ? L::mul(wgt, x) : x);
         }
       };
       if (IDMAP && jn == TJC) {
         // identity map: channel j is element j -- one tcgen05.ld.x32 fetches
         // the delay pairs of 16 consecutive channels
-        auto group = [&](const uint32_t(&r)[32], int h) {
+        auto group = [&](const uint32_t(&r)[32], const uint32_t(&w)[32], int h) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4) {
             const int4 k4 = MK4[(h + i) >> 2];
-            channel(((u64)r[2 * i + 1] << 32) | r[2 * i], (uint32_t)k4.x);
-            channel(((u64)r[2 * i + 3] << 32) | r[2 * i + 2], (uint32_t)k4.y);
-            channel(((u64)r[2 * i + 5] << 32) | r[2 * i + 4], (uint32_t)k4.z);
-            channel(((u64)r[2 * i + 7] << 32) | r[2 * i + 6], (uint32_t)k4.w);
+#define BM_PAIR(R, q) (((u64)R[2 * (i + q) + 1] << 32) | R[2 * (i + q)])
+            channel(BM_PAIR(r, 0), WT ? BM_PAIR(w, 0) : 0ull, (uint32_t)k4.x);
+            channel(BM_PAIR(r, 1), WT ? BM_PAIR(w, 1) : 0ull, (uint32_t)k4.y);
+            channel(BM_PAIR(r, 2), WT ? BM_PAIR(w, 2) : 0ull, (uint32_t)k4.z);
+            channel(BM_PAIR(r, 3), WT ? BM_PAIR(w, 3) : 0ull, (uint32_t)k4.w);
+#undef BM_PAIR
           }
         };
         const uint32_t tc = tlane + 2 * cur.cb * TJC;
 #pragma unroll
         for (int h = 0; h < TJC; h += 16) {
-          uint32_t r[32];
+          uint32_t r[32], w[32];
           tm_ld32_issue(tc + 2 * h, r);
-          tm_wait_regs(r);
-          group(r, h);
+          if (WT) {
+            tm_ld32_issue(tc + 2 * n_el + 2 * h, w);
+            tm_wait_regs2(r, w);
+          } else {
+            tm_wait_regs(r);
+          }
+          group(r, w, h);
         }
       } else {
         for (int jj = 0; jj < jn; ++jj) {
           const int m = IDMAP ? cur.cb * TJC + jj : MMc[jj];
-          channel((VT)tm_ld2(tlane + 2 * m), (uint32_t)MKc[jj]);
+          channel((VT)tm_ld2(tlane + 2 * m), WT ? (VT)tm_ld2(tlane + 2 * n_el + 2 * m) : 0ull,
+                  (uint32_t)MKc[jj]);
         }
       }
       // every gathered sample feeds acc: pinning acc before the arrive keeps
@@ -405,16 +447,30 @@ static int tma_window(const bm_das_geometry& g) {
   return g.rx_identity && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
 }
 
+// TMEM columns of one CTA: delay pairs (2 per element) plus, with
+// non-uniform apodisation, weight pairs (2 more per element)
+static int tma_cols(const bm_das_geometry& g) {
+  const int need = (g.uniform ? 2 : 4) * g.n_elements;
+  return need <= 256 ? 256 : 512;
+}
+
+// 128-channel stages exist for the uniform linear identity-map no-t0 kernels
+// (the BASELINE configurations): one stage boundary per 128 channels
+static bool tma_has128(const bm_das_geometry& g) {
+  return g.uniform && g.interp == BM_LINEAR && !g.t0_nonzero && g.rx_identity;
+}
+
 // channels per stage and stage count for the shared-memory share of one CTA
 static bool tma_plan(const bm_das_geometry& g, int& tjc, int& nst, size_t& smem) {
   const int W = tma_window(g);
-  const int per_sm = 2 * g.n_elements <= 256 ? 2 : 1;
+  const int per_sm = 512 / tma_cols(g);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   const bool pw = g.scheme == BM_PW;
-  const char* ev = getenv("BM_DAS_TJC");  // tuning override: 32 | 64
+  const char* ev = getenv("BM_DAS_TJC");  // tuning override: 32 | 64 | 128
   const int only = ev ? atoi(ev) : 0;
-  for (int t : {64, 32}) {
-    if (t == 64 && g.n_rx < 64) continue;
+  for (int t : {128, 64, 32}) {
+    if (t > g.n_rx && t > 32) continue;
+    if (t == 128 && !tma_has128(g)) continue;
     if (only && t != only) continue;
     int n = kTmaMaxStages;
     while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw).total > cap) --n;
@@ -429,7 +485,8 @@ static bool tma_plan(const bm_das_geometry& g, int& tjc, int& nst, size_t& smem)
 }
 
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
-  if (g.dtype != BM_F32 || !g.uniform || g.window_hint <= 0 || tma_window(g) > 256) return 0;
+  if (g.dtype != BM_F32 || g.window_hint <= 0 || tma_window(g) > 256) return 0;
+  if (!g.uniform && (4 * g.n_elements > 512 || (g.window == BM_HANN && !g.hann))) return 0;
   if (g.rx_identity && g.window_hint_g4 <= 0) return 0;  // 4-channel boxes need the bound
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;  // 16-B TMA strides
   if (2 * g.n_elements > 512) return 0;                       // pair layout in TMEM
@@ -461,8 +518,8 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
-  const int per_sm = 2 * g.n_elements <= 256 ? 2 : 1;
-  TmaArgs a{g, (float*)out, out_stride, n_frames, 1, W, nst, 2 * g.n_elements <= 256 ? 256 : 512};
+  const int per_sm = 512 / tma_cols(g);
+  TmaArgs a{g, (float*)out, out_stride, n_frames, 1, W, nst, tma_cols(g)};
   int fpc = 1;
   while (fpc < 16 && fpc * 2 <= n_frames &&
          (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
@@ -470,19 +527,32 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   a.frames_per_cta = fpc;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
-#define BM_TMA_ROW(J)                                                                         \
-  das_tma_kernel<false, false, false, false, J>, das_tma_kernel<false, false, false, true, J>, \
-      das_tma_kernel<false, false, true, false, J>, das_tma_kernel<false, false, true, true, J>, \
-      das_tma_kernel<false, true, false, false, J>, das_tma_kernel<false, true, false, true, J>, \
-      das_tma_kernel<false, true, true, false, J>, das_tma_kernel<false, true, true, true, J>,   \
-      das_tma_kernel<true, false, false, false, J>, das_tma_kernel<true, false, false, true, J>, \
-      das_tma_kernel<true, false, true, false, J>, das_tma_kernel<true, false, true, true, J>,   \
-      das_tma_kernel<true, true, false, false, J>, das_tma_kernel<true, true, false, true, J>,   \
-      das_tma_kernel<true, true, true, false, J>, das_tma_kernel<true, true, true, true, J>
-  static const kfn table[32] = {BM_TMA_ROW(32), BM_TMA_ROW(64)};
+#define BM_TMA_ROW(J, WT)                                                                  \
+  das_tma_kernel<false, false, false, false, J, WT>,                                        \
+      das_tma_kernel<false, false, false, true, J, WT>,                                     \
+      das_tma_kernel<false, false, true, false, J, WT>,                                     \
+      das_tma_kernel<false, false, true, true, J, WT>,                                      \
+      das_tma_kernel<false, true, false, false, J, WT>,                                     \
+      das_tma_kernel<false, true, false, true, J, WT>,                                      \
+      das_tma_kernel<false, true, true, false, J, WT>,                                      \
+      das_tma_kernel<false, true, true, true, J, WT>,                                       \
+      das_tma_kernel<true, false, false, false, J, WT>,                                     \
+      das_tma_kernel<true, false, false, true, J, WT>,                                      \
+      das_tma_kernel<true, false, true, false, J, WT>,                                      \
+      das_tma_kernel<true, false, true, true, J, WT>,                                       \
+      das_tma_kernel<true, true, false, false, J, WT>,                                      \
+      das_tma_kernel<true, true, false, true, J, WT>,                                       \
+      das_tma_kernel<true, true, true, false, J, WT>, das_tma_kernel<true, true, true, true, J, WT>
+  // rows: uniform/32, uniform/64, weighted/32, weighted/64
+  static const kfn table[64] = {BM_TMA_ROW(32, false), BM_TMA_ROW(64, false),
+                                BM_TMA_ROW(32, true), BM_TMA_ROW(64, true)};
 #undef BM_TMA_ROW
-  kfn k = table[(tjc == 64 ? 16 : 0) + ((pw ? 8 : 0) | (lin ? 4 : 0) |
-                                       (g.t0_nonzero ? 2 : 0) | (g.rx_identity ? 1 : 0))];
+  kfn k = table[(g.uniform ? 0 : 32) + (tjc >= 64 ? 16 : 0) +
+                ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) | (g.rx_identity ? 1 : 0))];
+  if (tjc == 128) {
+    if (!tma_has128(g)) return -1;
+    k = pw ? das_tma_kernel<true, true, false, true, 128> : das_tma_kernel<false, true, false, true, 128>;
+  }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return BM_ERR_CUDA;

@@ -87,6 +87,19 @@ __device__ __forceinline__ void tm_wait_regs(uint32_t (&r)[32]) {
                  "+r"(r[30]), "+r"(r[31])::"memory");
 }
 
+// wait::ld covering two x32 loads
+__device__ __forceinline__ void tm_wait_regs2(uint32_t (&r)[32], uint32_t (&w)[32]) {
+  tm_wait_regs(r);
+  // the first wait already retired every earlier tcgen05.ld of the thread;
+  // this empty asm only ties w's registers to a point after it
+  asm volatile("" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]),
+                    "+r"(w[6]), "+r"(w[7]), "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]),
+                    "+r"(w[12]), "+r"(w[13]), "+r"(w[14]), "+r"(w[15]), "+r"(w[16]), "+r"(w[17]),
+                    "+r"(w[18]), "+r"(w[19]), "+r"(w[20]), "+r"(w[21]), "+r"(w[22]), "+r"(w[23]),
+                    "+r"(w[24]), "+r"(w[25]), "+r"(w[26]), "+r"(w[27]), "+r"(w[28]), "+r"(w[29]),
+                    "+r"(w[30]), "+r"(w[31])::"memory");
+}
+
 // Lane arithmetic: a thread owns PAIR ? two pixels (packed f32x2) : one pixel.
 template <bool PAIR> struct Lane;
 template <> struct Lane<true> {

@@ -139,9 +139,10 @@ def test_no_contracted_fma_in_das_kernels():
     funcs = _sass_by_function()
     das = {n: l for n, l in funcs.items()
            if any(k in n for k in ("das_fast_kernel", "das_tmem_kernel", "das_tma_kernel"))}
-    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch, tma-32ch,
-    # tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0} x {identity map, general}
-    assert len(das) == 112
+    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch, tma-32ch, tma-64ch,
+    # weighted tma-32ch, weighted tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0}
+    # x {identity map, general} + 2 tma-128ch (uniform linear identity-map, STA | PW)
+    assert len(das) == 146
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
