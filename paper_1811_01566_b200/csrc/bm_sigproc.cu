@@ -285,11 +285,210 @@ static inline int ilog2(int64_t n) {
   return l;
 }
 
+
+// ---------------------------------------------------------------------------
+// f32 lanes of n = 32 * R samples (R = 8, 16, 32: n = 256 .. 1024), one WARP
+// per lane, data in REGISTERS.  With j = t + 32 i (t = lane, i < R) and
+// k = k1 + R k2:
+//   X[k1 + R k2] = sum_t W32^(t k2) * [ Wn^(t k1) * sum_i x[t + 32 i] WR^(i k1) ]
+// so a lane's transform is an R-point DFT inside each thread (radix-2 DIF,
+// compile-time register indices), a per-thread twiddle, and a 32-point DFT
+// across the warp (radix-2 DIF over __shfl_xor).  The spectrum ends up
+// bit-reversed in both indices, which the one-sided gain reads directly; the
+// inverse runs the mirror image (DIT across lanes, twiddle, DIT in registers)
+// and lands in natural order.  Shared memory holds only the twiddle table and
+// the CTA's [n][8] tile for coalesced 32-B row loads and stores: two
+// __syncthreads per CTA instead of one __syncwarp per radix-2 pass.
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ float2 c_mul(float2 a, float2 w) {
+  return {a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
+}
+__device__ __forceinline__ float2 c_conj(float2 a) { return {a.x, -a.y}; }
+
+template <int R>
+__device__ __forceinline__ int brev_c(int p) {  // bit reversal of p in log2(R) bits
+  int r = 0;
+#pragma unroll
+  for (int b = 1; b < R; b <<= 1) r = (r << 1) | ((p & b) ? 1 : 0);
+  return r;
+}
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restrict__ x,
+                                                           float* __restrict__ out,
+                                                           unsigned* __restrict__ peak,
+                                                           int64_t inner) {
+  constexpr int N = 32 * R, L = 8, LP = L + 1;  // LP: padded tile row (conflict-free columns)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);  // [N] Wn^m
+  float* tile = reinterpret_cast<float*>(tw + N);     // real: [N][LP]; complex: [N][LP] float2
+  const int tid = threadIdx.x, warp = tid >> 5, t = tid & 31;
+  const int64_t o = blockIdx.y, i_base = (int64_t)blockIdx.x * L;
+  const int lanes = (int)(inner - i_base < L ? inner - i_base : L);
+
+  for (int m = tid; m < N; m += 256) {
+    double sn, cs;
+    sincospi(-2.0 * (double)m / (double)N, &sn, &cs);
+    tw[m] = make_float2((float)cs, (float)sn);
+  }
+  const float* xo = x + o * (int64_t)N * inner + i_base;
+  for (int idx = tid; idx < N * L; idx += 256) {
+    const int l = idx & (L - 1), k = idx >> 3;
+    tile[k * LP + l] = l < lanes ? xo[(int64_t)k * inner + l] : 0.0f;
+  }
+  __syncthreads();
+
+  float2 v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = make_float2(tile[(t + 32 * i) * LP + warp], 0.0f);
+
+  // (1) R-point DFT over i in registers, radix-2 DIF: v[p] = A[brev(p)]
+#pragma unroll
+  for (int h = R / 2; h >= 1; h >>= 1)
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * h)
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float2 a = v[b + j], c = v[b + j + h];
+        v[b + j] = c_add(a, c);
+        v[b + j + h] = j == 0 ? c_sub(a, c) : c_mul(c_sub(a, c), tw[j * (N / (2 * h))]);
+      }
+  // (2) twiddle Wn^(t k1)
+#pragma unroll
+  for (int p = 1; p < R; ++p) v[p] = c_mul(v[p], tw[t * brev_c<R>(p)]);
+  // (3) 32-point DIF across the warp: lane t then holds k2 = brev5(t)
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = (t & h) != 0;
+    const float2 w = tw[(t & (h - 1)) * (N / (2 * h))];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      float2 q;
+      q.x = __shfl_xor_sync(0xffffffffu, v[p].x, h);
+      q.y = __shfl_xor_sync(0xffffffffu, v[p].y, h);
+      v[p] = up ? c_mul(c_sub(q, v[p]), w) : c_add(v[p], q);
+    }
+  }
+  // (4) one-sided gain (sigproc.py:63-70) at k = k1 + R k2
+  {
+    const int k2 = __brev(t) >> 27;
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      const int k = brev_c<R>(p) + R * k2;
+      const float gk = (k == 0 || k == N / 2) ? 1.0f : (k < N / 2 ? 2.0f : 0.0f);
+      v[p] = make_float2(v[p].x * gk, v[p].y * gk);
+    }
+  }
+  // (5) inverse 32-point DIT across the warp (bit-reversed in, natural out)
+#pragma unroll
+  for (int h = 1; h <= 16; h <<= 1) {
+    const bool up = (t & h) != 0;
+    const float2 w = c_conj(tw[(t & (h - 1)) * (N / (2 * h))]);
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      float2 q;
+      q.x = __shfl_xor_sync(0xffffffffu, v[p].x, h);
+      q.y = __shfl_xor_sync(0xffffffffu, v[p].y, h);
+      const float2 tmp = c_mul(up ? v[p] : q, w);
+      v[p] = up ? c_sub(q, tmp) : c_add(v[p], tmp);
+    }
+  }
+  // (6) twiddle Wn^(-t k1)
+#pragma unroll
+  for (int p = 1; p < R; ++p) v[p] = c_mul(v[p], c_conj(tw[t * brev_c<R>(p)]));
+  // (7) inverse R-point DIT in registers: v[i] = n * x'[t + 32 i]
+#pragma unroll
+  for (int h = 1; h < R; h <<= 1)
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * h)
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float2 a = v[b + j];
+        const float2 c = j == 0 ? v[b + j + h] : c_mul(v[b + j + h], c_conj(tw[j * (N / (2 * h))]));
+        v[b + j] = c_add(a, c);
+        v[b + j + h] = c_sub(a, c);
+      }
+
+  __syncthreads();  // tile reused for the output
+  const float inv_n = 1.0f / (float)N;
+  float vmax = 0.0f;
+  if (MODE == kComplex) {
+    float2* tc = reinterpret_cast<float2*>(tile);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      tc[(t + 32 * i) * LP + warp] = make_float2(v[i].x * inv_n, v[i].y * inv_n);
+  } else {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float e = magnitude(v[i].x * inv_n, v[i].y * inv_n);
+      tile[(t + 32 * i) * LP + warp] = e;
+      if (warp < lanes) vmax = e > vmax ? e : vmax;
+    }
+  }
+  __syncthreads();
+  const int64_t g0 = o * (int64_t)N * inner + i_base;
+  for (int idx = tid; idx < N * L; idx += 256) {
+    const int l = idx & (L - 1), k = idx >> 3;
+    if (l >= lanes) continue;
+    if (MODE == kComplex)
+      reinterpret_cast<float2*>(out)[g0 + (int64_t)k * inner + l] =
+          reinterpret_cast<const float2*>(tile)[k * LP + l];
+    else
+      out[g0 + (int64_t)k * inner + l] = tile[k * LP + l];
+  }
+  if (MODE == kEnvelope) block_peak<float>(vmax, peak + o);
+}
+
+template <typename T, int MODE>
+static int launch_analytic_reg(const T*, T*, typename PeakBits<T>::U*, int64_t, int64_t, int64_t,
+                               cudaStream_t) {
+  return -1;  // f64: shared-memory radix-2 kernel
+}
+template <>
+int launch_analytic_reg<float, kEnvelope>(const float*, float*, unsigned*, int64_t, int64_t,
+                                          int64_t, cudaStream_t);
+template <>
+int launch_analytic_reg<float, kComplex>(const float*, float*, unsigned*, int64_t, int64_t,
+                                         int64_t, cudaStream_t);
+
+template <int MODE>
+static int launch_reg_f32(const float* x, float* out, unsigned* peak, int64_t outer, int64_t n,
+                          int64_t inner, cudaStream_t s) {
+  const char* e = getenv("BM_FFT_KERNEL");  // "smem": the radix-2 shared-memory kernel
+  if (e && !strcmp(e, "smem")) return -1;
+  if (n != 256 && n != 512 && n != 1024) return -1;
+  if (inner > ((int64_t)1 << 34) || outer > 65535) return -1;
+  const size_t tile = (size_t)n * 9 * (MODE == kComplex ? 8 : 4);
+  const size_t smem = (size_t)n * 8 + tile;
+  auto k = n == 256 ? analytic_reg_kernel<MODE, 8>
+                    : (n == 512 ? analytic_reg_kernel<MODE, 16> : analytic_reg_kernel<MODE, 32>);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return BM_ERR_CUDA;
+  dim3 grid((unsigned)((inner + 7) / 8), (unsigned)outer);
+  k<<<grid, 256, smem, s>>>(x, out, peak, inner);
+  return cuda_status();
+}
+template <>
+int launch_analytic_reg<float, kEnvelope>(const float* x, float* out, unsigned* peak, int64_t outer,
+                                          int64_t n, int64_t inner, cudaStream_t s) {
+  return launch_reg_f32<kEnvelope>(x, out, peak, outer, n, inner, s);
+}
+template <>
+int launch_analytic_reg<float, kComplex>(const float* x, float* out, unsigned* peak, int64_t outer,
+                                         int64_t n, int64_t inner, cudaStream_t s) {
+  return launch_reg_f32<kComplex>(x, out, peak, outer, n, inner, s);
+}
+
 template <typename T, int MODE>
 static int launch_analytic(const T* x, T* out, typename PeakBits<T>::U* peak, int64_t outer,
                            int64_t n, int64_t inner, cudaStream_t s) {
   using V = typename C2<T>::type;
   if (outer > 65535) return BM_ERR_UNSUPPORTED;
+  {
+    const int rc = launch_analytic_reg<T, MODE>(x, out, peak, outer, n, inner, s);
+    if (rc >= 0) return rc;
+  }
   if (is_pow2(n)) {
     if (n > (1 << 20) || inner > (int64_t)1 << 40) return BM_ERR_UNSUPPORTED;
     const size_t lane_bytes = (size_t)n * sizeof(V);
