@@ -100,6 +100,12 @@ def sigproc():
         out[f"z32_{n}"] = ES.analytic_signal(x32, axis=0)
         out[f"x64_{n}"] = x64
         out[f"z64_{n}"] = ES.analytic_signal(x64, axis=0)
+    # wide images (37 lanes: a partial 8-lane CTA) at the register-FFT sizes
+    rng_w = np.random.default_rng(78)
+    for n in (256, 512, 1024):
+        xw = rng_w.normal(size=(n, 37)).astype(np.float32)
+        out[f"x32w_{n}"] = xw
+        out[f"z32w_{n}"] = ES.analytic_signal(xw, axis=0)
     e = np.abs(rng.normal(size=(64, 48))).astype(np.float32)
     e[3, 4] = 0.0
     out["dyn_in32"] = e
