@@ -22,6 +22,8 @@
  *                             dynamic_adjustment (sigproc.py:48-90), fused
  *   bm_display             <- the mapping half of dynamic_adjustment
  *                             (sigproc.py:91-97) given the peak
+ *   bm_fir_filter          <- fir_filter sigproc.py:36-45 (operator
+ *                             `fir_filter`, pipeline.py:96-105)
  */
 #ifndef BMODE200_H
 #define BMODE200_H
@@ -153,6 +155,13 @@ int bm_display(int32_t dtype, const void* e, const void* peak, void* disp, int32
 int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
                           int32_t* status, int32_t n_frames, int64_t frame_elems,
                           double range_db, void* stream);
+
+/* FIR pre-filter  <- sigproc.fir_filter sigproc.py:36-45 (lfilter(h, [1], x)),
+ * operator `fir_filter` pipeline.py:96-105.  x, y: [outer][n][inner] device
+ * arrays filtered along n; taps: device f64 [n_taps]; arithmetic in f64,
+ * y written in out_dtype.  BM_ERR_AXIS_TOO_SHORT if n < 1. */
+int bm_fir_filter(int32_t in_dtype, const void* x, int32_t out_dtype, void* y, int64_t outer,
+                  int64_t n, int64_t inner, const double* taps, int32_t n_taps, void* stream);
 
 const char* bm_error_string(int code);
 int bm_abi_version(void);

@@ -12,12 +12,12 @@ from . import engine, parallel
 from .engine import BmodeEngine
 from .environment import (Environment, Phantom, SimulatorSource, default_pw_angles,
                           open_simulator, simulate_rf, wire_phantom)
-from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,
+from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError, EmptyCoefficients,
                      InvalidMetadata, NativeError, NonPositiveRange, OperatorFailed, WrongStage)
 from .pipeline import (OPERATOR_REGISTRY, BenchmarkResult, OperatorKind, PipelineGraph,
                        StageTiming, benchmark, bmode_chain, build_graph, execute,
                        register_gpu_operators, register_operator)
-from .sigproc import analytic_signal, dynamic_adjustment, envelope
+from .sigproc import FirSpec, analytic_signal, dynamic_adjustment, envelope, fir_filter
 from .types import (AcquisitionContext, ApodizationSpec, BmodeImage, ImageGrid, PwScheme,
                     RfFrame, StaScheme, centered_rx_map, default_grid, validate_pair)
 

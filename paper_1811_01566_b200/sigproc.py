@@ -7,6 +7,9 @@ half of echopipe.sigproc (/root/reference/pkg/src/echopipe/sigproc.py:48-97).
 * ``envelope(z)``                   -- sigproc.py:76-78.
 * ``dynamic_adjustment(e, range_db)`` -- sigproc.py:81-97; returns float64
   like the reference (values computed in the input precision).
+* ``FirSpec`` / ``fir_filter(x, spec, axis=-1)`` -- sigproc.py:20-45, the RF
+  pre-filter: causal FIR with zero history, f64
+  arithmetic and f64 result like lfilter(h, [1.0], x); kernel ``bm_fir_filter``.
 
 Device policy as in beamform.py: numpy in -> numpy out; CUDA tensor in ->
 CUDA tensor out.  Kernels: ``bm_analytic_signal``, ``bm_envelope``,
@@ -21,7 +24,9 @@ import numpy as np
 
 from . import _native as N
 from ._device import to_device
-from .errors import AllZeroInput, AxisTooShort, NonPositiveRange
+from dataclasses import dataclass
+
+from .errors import AllZeroInput, AxisTooShort, EmptyCoefficients, NonPositiveRange
 from .types import _is_torch, _np_dtype
 
 
@@ -30,6 +35,74 @@ def _dev():
 
     N.require_cuda()
     return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass(frozen=True, eq=False)
+class FirSpec:
+    """FIR filter taps, applied causally along the sample axis (sigproc.py:20-33)."""
+
+    coefficients: np.ndarray
+
+    def __post_init__(self):
+        h = np.atleast_1d(np.asarray(self.coefficients, dtype=np.float64))
+        if h.size < 1:
+            raise EmptyCoefficients("FIR filter needs at least one coefficient")
+        if not np.all(np.isfinite(h)):
+            raise EmptyCoefficients("FIR coefficients must be finite")
+        h = h.reshape(-1).copy()
+        h.setflags(write=False)
+        object.__setattr__(self, "coefficients", h)
+
+
+def _fir_device(x, spec: FirSpec, axis: int, out_dtype):
+    """``y[n] = sum_m h[m] x[n - m]`` along ``axis`` of a device tensor, f64
+    arithmetic, result in ``out_dtype`` (torch dtype)."""
+    import torch
+
+    ax = axis % x.dim()
+    n = int(x.shape[ax])
+    if n < 1:
+        raise AxisTooShort("filter axis must have length >= 1")
+    x = x.contiguous()
+    shape = tuple(x.shape)
+    outer = int(np.prod(shape[:ax], dtype=np.int64))
+    inner = int(np.prod(shape[ax + 1:], dtype=np.int64))
+    y = torch.empty(shape, dtype=out_dtype, device=x.device)
+    if x.numel():
+        taps = torch.from_numpy(np.array(spec.coefficients, dtype=np.float64)).to(x.device)
+        code_in = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
+        code_out = N.BM_F32 if out_dtype == torch.float32 else N.BM_F64
+        with torch.cuda.device(x.device):
+            N.call("bm_fir_filter", code_in, x.data_ptr(), code_out, y.data_ptr(), outer, n, inner,
+                   taps.data_ptr(), int(taps.numel()), N.stream_ptr())
+    return y
+
+
+def fir_filter(x, spec: FirSpec, axis: int = -1):
+    """Causal FIR convolution ``y[n] = sum_m h[m] * x[n - m]`` (sigproc.py:36-45).
+
+    History before sample 0 is zero, so the output has the same length as the
+    input along ``axis``.  Like ``lfilter(h, [1.0], x)`` the arithmetic and the
+    result are float64 (the result type of f64 taps and a real frame)."""
+    import torch
+
+    is_t = _is_torch(x)
+    if not is_t:
+        x = np.asarray(x)
+    if x.ndim == 0:
+        x = x.reshape(1) if not is_t else x.reshape(1)
+    if int(x.shape[axis]) < 1:
+        raise AxisTooShort("filter axis must have length >= 1")
+    dt = np.dtype(_np_dtype(x))
+    if np.issubdtype(dt, np.complexfloating):
+        raise ValueError("fir_filter expects a real tensor")
+    dev = x.device if is_t and x.is_cuda else _dev()
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    xd = to_device(x, dev, tdt)
+    y = _fir_device(xd, spec, axis, torch.float64)
+    if is_t and x.is_cuda:
+        return y
+    return y.cpu().numpy()
 
 
 def _real_dtype_for(a):

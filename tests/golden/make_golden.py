@@ -16,6 +16,8 @@ Outputs:
                   six mid-size instances: rf, envelope, display arrays and the
                   complex analytic signal of two of them.
   sigproc.npz     analytic_signal / dynamic_adjustment on seeded arrays.
+  fir.npz         fir_filter (lfilter) on seeded f32/f64 traces, taps 1..64,
+                  along the sample axis and along axis 0 (inputs stored).
   configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
                   (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
                   N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
@@ -90,6 +92,26 @@ def chain():
     np.savez_compressed(os.path.join(HERE, "chain.npz"), **arrays)
 
 
+def fir():
+    """fir.npz: the reference's fir_filter (scipy lfilter) on seeded traces,
+    f32 and f64 frames, taps of 1..64, along the sample axis and axis 0."""
+    rng = np.random.default_rng(91)
+    out = {}
+    for nt in (1, 2, 7, 33, 64):
+        h = rng.normal(size=nt)
+        x32 = rng.normal(size=(3, 5, 300)).astype(np.float32)
+        x64 = rng.normal(size=(2, 4, 257))
+        out[f"h_{nt}"] = h
+        out[f"x32_{nt}"] = x32
+        out[f"y32_{nt}"] = ES.fir_filter(x32, ES.FirSpec(h))
+        out[f"x64_{nt}"] = x64
+        out[f"y64_{nt}"] = ES.fir_filter(x64, ES.FirSpec(h))
+        xa = rng.normal(size=(90, 6))
+        out[f"xa_{nt}"] = xa
+        out[f"ya_{nt}"] = ES.fir_filter(xa, ES.FirSpec(h), axis=0)
+    np.savez_compressed(os.path.join(HERE, "fir.npz"), **out)
+
+
 def sigproc():
     rng = np.random.default_rng(77)
     out = {}
@@ -151,7 +173,7 @@ def configs():
 
 
 if __name__ == "__main__":
-    for fn in (das_small, chain, sigproc, configs):
+    for fn in (das_small, chain, sigproc, fir, configs):
         t = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)

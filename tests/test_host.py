@@ -112,9 +112,23 @@ def test_graph_building_like_reference():
 def test_register_into_foreign_registry():
     reg = {}
     kinds = bm.register_gpu_operators(registry=reg)
-    assert sorted(reg) == ["analytic_signal", "beamform", "dynamic_adjustment", "envelope"]
-    assert {k.name: (k.input_kinds, k.output_kind) for k in kinds}["beamform"] == (
-        ("observation",), "rf_image")
+    assert sorted(reg) == ["analytic_signal", "beamform", "dynamic_adjustment", "envelope",
+                           "fir_filter"]
+    ports = {k.name: (k.input_kinds, k.output_kind) for k in kinds}
+    assert ports["beamform"] == (("observation",), "rf_image")
+    assert ports["fir_filter"] == (("observation",), "observation")  # pipeline.py:209
+
+
+def test_fir_spec_validation():
+    """FirSpec mirrors sigproc.py:20-33: f64, read-only, EmptyCoefficients for
+    empty or non-finite taps (test_sigproc.py:55-61)."""
+    from paper_1811_01566_b200.errors import EmptyCoefficients
+
+    spec = bm.FirSpec([1, 2, 3])
+    assert spec.coefficients.dtype == np.float64 and not spec.coefficients.flags.writeable
+    for bad in ([], [1.0, np.nan], [np.inf]):
+        with pytest.raises(EmptyCoefficients):
+            bm.FirSpec(bad)
 
 
 def _sass_by_function():

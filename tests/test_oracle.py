@@ -96,3 +96,16 @@ def test_oracle_thread_count_bits():
     a = O.das_beamform(data, ctx, grid, n_threads=1)
     b = O.das_beamform(data, ctx, grid, n_threads=3)
     assert a.tobytes() == b.tobytes()
+
+
+def test_fir_oracle_matches_reference_goldens(golden_dir):
+    """oracle.fir_filter (np.convolve in f64, lfilter's one-term-denominator
+    branch) reproduces the reference's fir_filter bits."""
+    g = np.load(os.path.join(golden_dir, "fir.npz"))
+    for nt in (1, 2, 7, 33, 64):
+        h = g[f"h_{nt}"]
+        for xk, yk, ax in (("x32", "y32", -1), ("x64", "y64", -1), ("xa", "ya", 0)):
+            y = O.fir_filter(g[f"{xk}_{nt}"], h, axis=ax)
+            ref = g[f"{yk}_{nt}"]
+            assert y.dtype == ref.dtype == np.float64
+            assert np.array_equal(y, ref), (nt, xk)
