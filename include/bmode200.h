@@ -24,6 +24,9 @@
  *                             (sigproc.py:91-97) given the peak
  *   bm_fir_filter          <- fir_filter sigproc.py:36-45 (operator
  *                             `fir_filter`, pipeline.py:96-105)
+ *   bm_sliding_moments     <- qus.sliding_moments qus.py:122-158
+ *   bm_dense_forward       <- qus.dense_forward qus.py:170-183 (with the
+ *                             moments: estimate_hk_map qus.py:186-192)
  */
 #ifndef BMODE200_H
 #define BMODE200_H
@@ -162,6 +165,20 @@ int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* dis
  * y written in out_dtype.  BM_ERR_AXIS_TOO_SHORT if n < 1. */
 int bm_fir_filter(int32_t in_dtype, const void* x, int32_t out_dtype, void* y, int64_t outer,
                   int64_t n, int64_t inner, const double* taps, int32_t n_taps, void* stream);
+
+/* Sliding-window moments  <- qus.sliding_moments qus.py:122-158.  img: device
+ * [n_rows][n_cols] (f32 or f64, widened to f64); m1/m2/m3: device f64
+ * [(n_rows-wh)/sh + 1][(n_cols-ww)/sw + 1], means of x, x^2, x^3. */
+int bm_sliding_moments(int32_t dtype, const void* img, int64_t n_rows, int64_t n_cols,
+                       int32_t wh, int32_t ww, int32_t sh, int32_t sw, double* m1, double* m2,
+                       double* m3, void* stream);
+
+/* Dense homodyned-K model  <- qus.dense_forward qus.py:170-183.  x: device f64
+ * [n][in0]; params: device f64, per layer W (out x in, row-major) then b;
+ * dims: device int32 [n_layers][3] = {in, out, activation (0 relu, 1 identity,
+ * 2 softplus)}; max_width >= every layer width; y: device f64 [n][out_last]. */
+int bm_dense_forward(const double* x, int64_t n, const double* params, const int32_t* dims,
+                     int32_t n_layers, int32_t max_width, double* y, void* stream);
 
 const char* bm_error_string(int code);
 int bm_abi_version(void);

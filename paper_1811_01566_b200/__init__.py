@@ -8,15 +8,18 @@ Public names mirror echopipe/__init__.py:9-64 for the path.
 """
 
 from .beamform import INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform
-from . import engine, parallel
+from . import engine, parallel, qus
 from .engine import BmodeEngine
 from .environment import (Environment, Phantom, SimulatorSource, default_pw_angles,
                           open_simulator, simulate_rf, wire_phantom)
-from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError, EmptyCoefficients,
-                     InvalidMetadata, NativeError, NonPositiveRange, OperatorFailed, WrongStage)
+from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,
+                     EmptyCoefficients, FormatError, InvalidMetadata, NativeError,
+                     NonPositiveRange, OperatorFailed, WindowTooLarge, WrongStage)
 from .pipeline import (OPERATOR_REGISTRY, BenchmarkResult, OperatorKind, PipelineGraph,
                        StageTiming, benchmark, bmode_chain, build_graph, execute,
                        register_gpu_operators, register_operator)
+from .qus import (DenseLayer, DenseModel, HkParamsMap, MomentMaps, dense_forward,
+                  estimate_hk_map, load_model, save_model, sliding_moments)
 from .sigproc import FirSpec, analytic_signal, dynamic_adjustment, envelope, fir_filter
 from .types import (AcquisitionContext, ApodizationSpec, BmodeImage, ImageGrid, PwScheme,
                     RfFrame, StaScheme, centered_rx_map, default_grid, validate_pair)

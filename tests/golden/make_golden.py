@@ -18,6 +18,8 @@ Outputs:
   sigproc.npz     analytic_signal / dynamic_adjustment on seeded arrays.
   fir.npz         fir_filter (lfilter) on seeded f32/f64 traces, taps 1..64,
                   along the sample axis and along axis 0 (inputs stored).
+  qus.npz         sliding_moments / estimate_hk_map on seeded Rayleigh
+                  envelopes with a seeded relu/softplus/identity model.
   configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
                   (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
                   N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
@@ -112,6 +114,33 @@ def fir():
     np.savez_compressed(os.path.join(HERE, "fir.npz"), **out)
 
 
+def qus():
+    """qus.npz: the reference's sliding_moments / estimate_hk_map on seeded
+    Rayleigh envelopes with a seeded 3-layer model (inputs stored)."""
+    from echopipe import qus as EQ
+
+    rng = np.random.default_rng(303)
+    out = {}
+    cases = [((64, 48), (8, 4), (4, 2)), ((97, 31), (5, 5), (1, 1)),
+             ((512, 40), (64, 4), (32, 2)), ((33, 33), (33, 33), (1, 1))]
+    layers = [(rng.normal(size=(8, 3)), rng.normal(size=8), "relu"),
+              (rng.normal(size=(6, 8)), rng.normal(size=6), "softplus"),
+              (rng.normal(size=(2, 6)), rng.normal(size=2), "identity")]
+    model = EQ.DenseModel(tuple(EQ.DenseLayer(w, b, a) for w, b, a in layers))
+    for i, (shape, win, st) in enumerate(cases):
+        img = rng.rayleigh(1.0, size=shape).astype(np.float32 if i % 2 else np.float64)
+        m = EQ.sliding_moments(img, win, st)
+        hk = EQ.estimate_hk_map(img, win, st, model)
+        out[f"img_{i}"] = img
+        out[f"win_{i}"], out[f"stride_{i}"] = np.array(win), np.array(st)
+        out[f"m1_{i}"], out[f"m2_{i}"], out[f"m3_{i}"] = m.m1, m.m2, m.m3
+        out[f"u_{i}"], out[f"k_{i}"] = hk.u, hk.k
+    for j, (w, b, a) in enumerate(layers):
+        out[f"W_{j}"], out[f"b_{j}"] = w, b
+    out["acts"] = np.array([a for _, _, a in layers])
+    np.savez_compressed(os.path.join(HERE, "qus.npz"), **out)
+
+
 def sigproc():
     rng = np.random.default_rng(77)
     out = {}
@@ -173,7 +202,7 @@ def configs():
 
 
 if __name__ == "__main__":
-    for fn in (das_small, chain, sigproc, fir, configs):
+    for fn in (das_small, chain, sigproc, fir, qus, configs):
         t = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)

@@ -113,10 +113,12 @@ def test_register_into_foreign_registry():
     reg = {}
     kinds = bm.register_gpu_operators(registry=reg)
     assert sorted(reg) == ["analytic_signal", "beamform", "dynamic_adjustment", "envelope",
-                           "fir_filter"]
+                           "fir_filter", "hk_estimator", "sliding_moments"]
     ports = {k.name: (k.input_kinds, k.output_kind) for k in kinds}
     assert ports["beamform"] == (("observation",), "rf_image")
     assert ports["fir_filter"] == (("observation",), "observation")  # pipeline.py:209
+    assert ports["sliding_moments"] == (("envelope_image",), "moment_maps")  # :221-225
+    assert ports["hk_estimator"] == (("envelope_image",), "hk_map")  # :226-228
 
 
 def test_fir_spec_validation():

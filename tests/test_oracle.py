@@ -109,3 +109,16 @@ def test_fir_oracle_matches_reference_goldens(golden_dir):
             ref = g[f"{yk}_{nt}"]
             assert y.dtype == ref.dtype == np.float64
             assert np.array_equal(y, ref), (nt, xk)
+
+
+def test_qus_oracle_matches_reference_goldens(golden_dir):
+    """oracle.sliding_moments / dense_forward reproduce the reference's
+    qus outputs bit for bit (same numpy operations)."""
+    g = np.load(os.path.join(golden_dir, "qus.npz"))
+    layers = [(g[f"W_{j}"], g[f"b_{j}"], str(a)) for j, a in enumerate(g["acts"])]
+    for i in range(4):
+        m1, m2, m3 = O.sliding_moments(g[f"img_{i}"], tuple(g[f"win_{i}"]), tuple(g[f"stride_{i}"]))
+        assert np.array_equal(m1, g[f"m1_{i}"]) and np.array_equal(m2, g[f"m2_{i}"])
+        assert np.array_equal(m3, g[f"m3_{i}"])
+        out = O.dense_forward(np.stack([m1, m2, m3], axis=-1), layers)
+        assert np.array_equal(out[..., 0], g[f"u_{i}"]) and np.array_equal(out[..., 1], g[f"k_{i}"])
