@@ -27,6 +27,7 @@
  *   bm_sliding_moments     <- qus.sliding_moments qus.py:122-158
  *   bm_dense_forward       <- qus.dense_forward qus.py:170-183 (with the
  *                             moments: estimate_hk_map qus.py:186-192)
+ *   bm_quantize_u8         <- the pixel mapping of write_pgm formats.py:189-200
  */
 #ifndef BMODE200_H
 #define BMODE200_H
@@ -179,6 +180,10 @@ int bm_sliding_moments(int32_t dtype, const void* img, int64_t n_rows, int64_t n
  * 2 softplus)}; max_width >= every layer width; y: device f64 [n][out_last]. */
 int bm_dense_forward(const double* x, int64_t n, const double* params, const int32_t* dims,
                      int32_t n_layers, int32_t max_width, double* y, void* stream);
+
+/* Display -> 8-bit PGM pixels  <- write_pgm formats.py:189-200:
+ * out[i] = floor(disp[i] * 255 + 0.5), rounded in the display dtype. */
+int bm_quantize_u8(int32_t dtype, const void* disp, uint8_t* out, int64_t count, void* stream);
 
 const char* bm_error_string(int code);
 int bm_abi_version(void);

@@ -10,8 +10,10 @@ Public names mirror echopipe/__init__.py:9-64 for the path.
 from .beamform import INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform
 from . import engine, parallel, qus
 from .engine import BmodeEngine
-from .environment import (Environment, Phantom, SimulatorSource, default_pw_angles,
-                          open_simulator, simulate_rf, wire_phantom)
+from .environment import (DatasetSource, Environment, Phantom, SimulatorSource,
+                          default_pw_angles, open_dataset, open_simulator, simulate_rf,
+                          wire_phantom)
+from .formats import WfrfReader, read_wfrf, write_pgm, write_wfrf
 from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,
                      EmptyCoefficients, FormatError, InvalidMetadata, NativeError,
                      NonPositiveRange, OperatorFailed, WindowTooLarge, WrongStage)

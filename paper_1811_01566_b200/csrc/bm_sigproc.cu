@@ -631,3 +631,32 @@ extern "C" const char* bm_error_string(int code) {
 }
 
 extern "C" int bm_abi_version(void) { return BMODE200_ABI_VERSION; }
+
+// Display -> 8-bit pixels for PGM output (formats.py:189-200):
+// floor(v * 255 + 0.5) with each operator rounded in the display dtype, as
+// numpy evaluates it (a weak python scalar keeps f32 arrays in f32).
+namespace bm {
+template <typename T>
+__global__ void quantize_u8_kernel(const T* __restrict__ d, uint8_t* __restrict__ out, int64_t n) {
+  using O = R<T>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T s = O::add(O::mul(d[i], T(255)), T(0.5));
+    out[i] = (uint8_t)floor(s);
+  }
+}
+}  // namespace bm
+
+extern "C" int bm_quantize_u8(int32_t dtype, const void* disp, uint8_t* out, int64_t count,
+                              void* stream) {
+  if (!disp || !out || count < 0) return BM_ERR_INVALID_ARGUMENT;
+  if (count == 0) return BM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == BM_F32)
+    quantize_u8_kernel<float><<<grid_for(count), 256, 0, s>>>((const float*)disp, out, count);
+  else if (dtype == BM_F64)
+    quantize_u8_kernel<double><<<grid_for(count), 256, 0, s>>>((const double*)disp, out, count);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}

@@ -128,18 +128,23 @@ class BmodeEngine:
         self.reconstruct_host_stream([(rf_host, disp_host)], chunk=chunk)
         return disp_host
 
-    def reconstruct_host_stream(self, batches, chunk: int = 8):
+    def reconstruct_host_stream(self, batches, chunk: int = 8, on_uploaded=None):
         """A stream of host batches ``[(rf_host, disp_host), ...]`` reconstructed
         as one continuous chunk pipeline (H2D of chunk i+1 and D2H of chunk
         i-1 overlap the reconstruction of chunk i, across batch boundaries),
         synchronising once at the end.  Every batch's RF is copied in and its
-        display copied out."""
+        display copied out.
+
+        ``batches`` may be a lazy iterable; ``on_uploaded(i, event)`` is called
+        once batch i's H2D copies are enqueued -- the batch's host RF buffer
+        may be refilled after ``event`` completes."""
         import torch
 
-        batches = list(batches)
-        if not batches:
+        it = iter(batches)
+        first = next(it, None)
+        if first is None:
             return
-        n_s = int(batches[0][0].shape[-1])
+        n_s = int(first[0].shape[-1])
         chunk = max(1, chunk)
         nbuf = 3
         key = ("host", chunk, n_s)
@@ -155,13 +160,17 @@ class BmodeEngine:
         up_done = [None] * nbuf
         comp_done = [None] * nbuf
         down_done = [None] * nbuf
-        total = sum(int(rf.shape[0]) for rf, _ in batches)
-        status = torch.zeros(total, dtype=torch.int32, device=self.device)
-        self._last_status = status
+        statuses = []
         i = 0
-        base = 0
-        for rf_host, disp_host in batches:
+
+        def batches_all():
+            yield first
+            yield from it
+
+        for b, (rf_host, disp_host) in enumerate(batches_all()):
             f = int(rf_host.shape[0])
+            status = torch.zeros(f, dtype=torch.int32, device=self.device)
+            statuses.append(status)
             for lo in range(0, f, chunk):
                 hi = min(f, lo + chunk)
                 slot = i % nbuf
@@ -175,7 +184,7 @@ class BmodeEngine:
                 if down_done[slot] is not None:
                     comp.wait_event(down_done[slot])  # slot's output buffer drained
                 self.reconstruct(bufs[slot][: hi - lo], out=outs[slot][: hi - lo], stream=comp,
-                                 key=("host", chunk), status=status[base + lo:base + hi])
+                                 key=("host", chunk), status=status[lo:hi])
                 comp_done[slot] = torch.cuda.Event()
                 comp_done[slot].record(comp)
                 with torch.cuda.stream(d2h):
@@ -184,6 +193,83 @@ class BmodeEngine:
                     down_done[slot] = torch.cuda.Event()
                     down_done[slot].record(d2h)
                 i += 1
-            base += f
+            if on_uploaded is not None:
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                on_uploaded(b, ev)
+        self._last_status = torch.cat(statuses) if len(statuses) > 1 else statuses[0]
         d2h.synchronize()
         comp.synchronize()
+
+    def reconstruct_file(self, path, batch: int = 32, chunk: int = 8):
+        """B-mode displays of every frame of a WFRF file.
+
+        A reader thread fills two pinned host batches straight from the file
+        (``WfrfReader.read_into``), so disk reads overlap the H2D copies and
+        the reconstruction of the previous batch; the chunk pipeline of
+        :meth:`reconstruct_host_stream` overlaps copies and compute on the
+        GPU.  Returns (pinned display tensor [n_frames, n_z, n_x], context)."""
+        import queue
+        import threading
+
+        import torch
+
+        from .formats import WfrfReader
+
+        rd = WfrfReader(path)
+        try:
+            if rd.frame_count == 0:
+                return torch.empty((0,) + self.image_shape, dtype=self.tdtype), rd.context
+            shape = tuple(rd.frame_shape)
+            native = np.dtype(rd.dtype.newbyteorder("="))
+            if shape[:2] != tuple(self.frame_shape) or native != self.dtype:
+                from .errors import DimensionMismatch
+
+                raise DimensionMismatch(0, f"file frames {shape} {rd.dtype} do not match the "
+                                           f"engine's {self.frame_shape} {np.dtype(self.dtype)}")
+            n_s = shape[2]
+            disp = torch.empty((rd.frame_count,) + self.image_shape, dtype=self.tdtype,
+                               pin_memory=True)
+            free = queue.Queue()
+            filled = queue.Queue(maxsize=2)
+            for _ in range(2):
+                free.put((torch.empty((batch,) + shape, dtype=self.tdtype, pin_memory=True),
+                          None))
+            failure = []
+
+            def reader():
+                try:
+                    lo = 0
+                    while lo < rd.frame_count:
+                        buf, ev = free.get()
+                        if ev is not None:
+                            ev.synchronize()  # the GPU has copied this buffer out
+                        k = rd.read_into(buf)
+                        filled.put((buf, lo, k))
+                        lo += k
+                except Exception as exc:  # surfaced on the consumer side
+                    failure.append(exc)
+                filled.put(None)
+
+            th = threading.Thread(target=reader, daemon=True)
+            th.start()
+            bufs_in_flight = {}
+
+            def batches():
+                b = 0
+                while (item := filled.get()) is not None:
+                    buf, lo, k = item
+                    bufs_in_flight[b] = buf
+                    b += 1
+                    yield buf[:k], disp[lo:lo + k]
+
+            def recycle(b, ev):
+                free.put((bufs_in_flight.pop(b), ev))
+
+            self.reconstruct_host_stream(batches(), chunk=chunk, on_uploaded=recycle)
+            th.join()
+            if failure:
+                raise failure[0]
+            return disp, rd.context
+        finally:
+            rd.close()

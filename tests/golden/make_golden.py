@@ -20,6 +20,9 @@ Outputs:
                   along the sample axis and along axis 0 (inputs stored).
   qus.npz         sliding_moments / estimate_hk_map on seeded Rayleigh
                   envelopes with a seeded relu/softplus/identity model.
+  ref_small.wfrf, ref_pw.wfrf
+                  WFRF files written by the reference (STA f32 with t0; PW f64
+                  with an rx map); pgm.npz: write_pgm bytes of seeded displays.
   configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
                   (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
                   N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
@@ -141,6 +144,35 @@ def qus():
     np.savez_compressed(os.path.join(HERE, "qus.npz"), **out)
 
 
+def formats():
+    """ref_small.wfrf / ref_pw.wfrf written by the reference's write_wfrf, and
+    pgm.npz: write_pgm bytes of seeded display images (f32 and f64)."""
+    from echopipe import formats as EF
+    from echopipe.types import (AcquisitionContext, BmodeImage, ImageGrid, PwScheme, RfFrame,
+                                StaScheme)
+
+    rng = np.random.default_rng(404)
+    ctx = AcquisitionContext(1540.0, 20e6, 4, 3e-4, StaScheme((0, 1, 2, 3)),
+                             time_zero_offset=np.linspace(0, 1e-6, 4))
+    frames = [RfFrame(rng.normal(size=(4, 4, 32)).astype(np.float32)) for _ in range(3)]
+    EF.write_wfrf(os.path.join(HERE, "ref_small.wfrf"), frames, ctx)
+    ctx = AcquisitionContext(1540.0, 40e6, 6, 2e-4, PwScheme((-0.1, 0.0, 0.1)),
+                             rx_channel_map=np.array([[0, 2, 4], [1, 3, 5], [5, 4, 3]]))
+    frames = [RfFrame(rng.normal(size=(3, 3, 16))) for _ in range(2)]
+    EF.write_wfrf(os.path.join(HERE, "ref_pw.wfrf"), frames, ctx)
+    out = {}
+    for name, dt in (("f32", np.float32), ("f64", np.float64)):
+        d = rng.random((37, 29)).astype(dt)
+        d[0, :6] = np.array([0.0, 1.0, 0.5, 0.5 / 255, 1.5 / 255, 254.5 / 255], dtype=dt)
+        img = BmodeImage(d, stage="display", grid=ImageGrid(np.arange(29) * 1e-4,
+                                                             np.arange(37) * 1e-4))
+        path = os.path.join("/tmp", f"golden_{name}.pgm")
+        EF.write_pgm(img, path)
+        out[f"disp_{name}"] = d
+        out[f"pgm_{name}"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "pgm.npz"), **out)
+
+
 def sigproc():
     rng = np.random.default_rng(77)
     out = {}
@@ -202,7 +234,7 @@ def configs():
 
 
 if __name__ == "__main__":
-    for fn in (das_small, chain, sigproc, fir, qus, configs):
+    for fn in (das_small, chain, sigproc, fir, qus, formats, configs):
         t = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)
