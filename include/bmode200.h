@@ -28,6 +28,7 @@
  *   bm_dense_forward       <- qus.dense_forward qus.py:170-183 (with the
  *                             moments: estimate_hk_map qus.py:186-192)
  *   bm_quantize_u8         <- the pixel mapping of write_pgm formats.py:189-200
+ *   bm_simulate_rf         <- simulate_rf environment.py:91-129 (synthetic RF)
  */
 #ifndef BMODE200_H
 #define BMODE200_H
@@ -184,6 +185,17 @@ int bm_dense_forward(const double* x, int64_t n, const double* params, const int
 /* Display -> 8-bit PGM pixels  <- write_pgm formats.py:189-200:
  * out[i] = floor(disp[i] * 255 + 0.5), rounded in the display dtype. */
 int bm_quantize_u8(int32_t dtype, const void* disp, uint8_t* out, int64_t count, void* stream);
+
+/* RF simulator  <- environment.simulate_rf environment.py:91-129.  Device
+ * arrays: elem_x f64 [n_el]; tx_elements int32 [n_tx] (STA) or cos_a/sin_a
+ * f64 [n_tx] (PW, evaluated on the host); rx_map int32 [n_tx][n_rx];
+ * t0 f64 [n_tx] seconds; scatterers f64 [n][3] (x, z, amplitude).
+ * out: [n_tx][n_rx][n_samples] in out_dtype (f64 sums, one final rounding). */
+int bm_simulate_rf(int32_t scheme, int32_t n_tx, int32_t n_rx, int32_t n_samples,
+                   const double* elem_x, const int32_t* tx_elements, const double* cos_a,
+                   const double* sin_a, const int32_t* rx_map, const double* t0, double c,
+                   double fs, double center_frequency, double n_cycles, const double* scatterers,
+                   int32_t n_scatterers, int32_t out_dtype, void* out, void* stream);
 
 const char* bm_error_string(int code);
 int bm_abi_version(void);

@@ -12,7 +12,7 @@ from . import engine, parallel, qus
 from .engine import BmodeEngine
 from .environment import (DatasetSource, Environment, Phantom, SimulatorSource,
                           default_pw_angles, open_dataset, open_simulator, simulate_rf,
-                          wire_phantom)
+                          simulate_rf_device, wire_phantom)
 from .formats import WfrfReader, read_wfrf, write_pgm, write_wfrf
 from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,
                      EmptyCoefficients, FormatError, InvalidMetadata, NativeError,

@@ -56,6 +56,8 @@ SIGNATURES = {
                            ctypes.c_int),
     "bm_dense_forward": ([_P, _I64, _P, _P, _I32, _I32, _P, _P], ctypes.c_int),
     "bm_quantize_u8": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
+    "bm_simulate_rf": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _I32,
+                        _I32, _P, _P], ctypes.c_int),
     "bm_frame_peak": ([_I32, _P, _P, _I32, _I64, _P], ctypes.c_int),
     "bm_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
     "bm_dynamic_adjustment": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),

@@ -23,6 +23,8 @@ Outputs:
   ref_small.wfrf, ref_pw.wfrf
                   WFRF files written by the reference (STA f32 with t0; PW f64
                   with an rx map); pgm.npz: write_pgm bytes of seeded displays.
+  sim.npz         simulate_rf (noise-free): f64 STA (t0, rx map) and PW frames,
+                  sha256 of the cfg2 wire-phantom f32 frame.
   configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
                   (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
                   N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
@@ -173,6 +175,31 @@ def formats():
     np.savez_compressed(os.path.join(HERE, "pgm.npz"), **out)
 
 
+def sim():
+    """sim.npz: the reference's simulate_rf (noise-free) -- f64 frames of a
+    small STA case (t0 offsets, rx map) and a small PW case, and the sha256 of
+    the cfg2 wire-phantom frame in f32 (the benchmark cine's clean signal)."""
+    from echopipe.types import AcquisitionContext as AC, PwScheme as PS, StaScheme as SS
+
+    from paper_1811_01566_b200 import environment as ME
+
+    ph = EE.Phantom(((0.4e-3, 4.9e-3, 1.0), (-1.1e-3, 7.3e-3, 0.6), (2.0e-3, 3.1e-3, -0.8)),
+                    center_frequency=5e6, n_cycles=2)
+    out = {}
+    ctx = AC(1540.0, 40e6, 16, 2e-4, SS((0, 5, 11, 15)),
+             rx_channel_map=np.array([[i, (i + 3) % 16, 15 - i] for i in (0, 5, 11, 15)]),
+             time_zero_offset=np.array([0.0, 1e-7, -2e-7, 3.3e-7]))
+    out["sta_f64"] = EE.simulate_rf(ph, ctx, 600, dtype=np.float64).data
+    ctx = AC(1480.0, 31.25e6, 24, 3e-4, PS((-0.2, 0.05, 0.17)))
+    out["pw_f64"] = EE.simulate_rf(ph, ctx, 500, dtype=np.float64).data
+    ctx_m, grid_m, n_s = ME.config_geometry("cfg2")
+    ctx = AC(ctx_m.speed_of_sound, ctx_m.sampling_frequency, ctx_m.n_elements, ctx_m.pitch,
+             PS(ctx_m.tx_scheme.angles_rad))
+    clean = EE.simulate_rf(EP.wire_phantom(), ctx, n_s, dtype=np.float32).data
+    out["cfg2_wire_f32_sha256"] = np.array(hashlib.sha256(clean.tobytes()).hexdigest())
+    np.savez_compressed(os.path.join(HERE, "sim.npz"), **out)
+
+
 def sigproc():
     rng = np.random.default_rng(77)
     out = {}
@@ -234,7 +261,7 @@ def configs():
 
 
 if __name__ == "__main__":
-    for fn in (das_small, chain, sigproc, fir, qus, formats, configs):
+    for fn in (das_small, chain, sigproc, fir, qus, formats, sim, configs):
         t = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)

@@ -122,3 +122,21 @@ def test_qus_oracle_matches_reference_goldens(golden_dir):
         assert np.array_equal(m3, g[f"m3_{i}"])
         out = O.dense_forward(np.stack([m1, m2, m3], axis=-1), layers)
         assert np.array_equal(out[..., 0], g[f"u_{i}"]) and np.array_equal(out[..., 1], g[f"k_{i}"])
+
+
+def test_host_simulator_matches_reference_sim_goldens(golden_dir):
+    """The host restatement of simulate_rf (the bench's input generator and
+    the GPU simulator's checker) reproduces the reference bit for bit."""
+    g = np.load(os.path.join(golden_dir, "sim.npz"))
+    ph = ME.Phantom(((0.4e-3, 4.9e-3, 1.0), (-1.1e-3, 7.3e-3, 0.6), (2.0e-3, 3.1e-3, -0.8)),
+                    center_frequency=5e6, n_cycles=2)
+    ctx = T.AcquisitionContext(1540.0, 40e6, 16, 2e-4, T.StaScheme((0, 5, 11, 15)),
+                               rx_channel_map=np.array([[i, (i + 3) % 16, 15 - i]
+                                                        for i in (0, 5, 11, 15)]),
+                               time_zero_offset=np.array([0.0, 1e-7, -2e-7, 3.3e-7]))
+    assert np.array_equal(ME.simulate_rf(ph, ctx, 600, np.float64).data, g["sta_f64"])
+    ctx = T.AcquisitionContext(1480.0, 31.25e6, 24, 3e-4, T.PwScheme((-0.2, 0.05, 0.17)))
+    assert np.array_equal(ME.simulate_rf(ph, ctx, 500, np.float64).data, g["pw_f64"])
+    ctx, grid, n_s = ME.config_geometry("cfg2")
+    clean = ME.simulate_rf(ME.wire_phantom(), ctx, n_s, np.float32).data
+    assert hashlib.sha256(clean.tobytes()).hexdigest() == str(g["cfg2_wire_f32_sha256"])
