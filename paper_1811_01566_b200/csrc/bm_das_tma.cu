@@ -44,14 +44,14 @@ struct TmaArgs {
 // shared-memory carve (bytes), identical on host and device
 struct TmaLayout {
   int tmin, rmin, metaK, metaM, txd, win, total;
-  __host__ __device__ TmaLayout(int n_tx, int n_el, int tjc, int nst, int W, bool pw) {
+  __host__ __device__ TmaLayout(int n_tx, int n_el, int tjc, int nst, int W, bool pw, int fp) {
     tmin = 256;  // [0,16) TMEM base, [64,128) full barriers, [128,192) empty barriers
     rmin = (tmin + 16 * n_tx + 15) & ~15;
     metaK = (rmin + 8 * n_el + 15) & ~15;
-    metaM = metaK + 4 * tjc * nst;
+    metaM = metaK + 4 * tjc * nst * fp;
     txd = metaM + 4 * tjc * nst;
     win = (txd + (pw ? n_tx * 128 * 8 : 0) + 127) & ~127;
-    total = win + nst * tjc * W * 4;
+    total = win + nst * tjc * fp * W * 4;
   }
 };
 
@@ -100,19 +100,26 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // per-pixel weights w[m] live in TMEM next to the delays (columns
 // 2*n_el + 2m, 2m+1), and a contribution is acc + (w*(1-a))*x0 + (w*a)*x1
 // exactly as beamform.py:175-187 rounds it.
-template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false>
-__global__ void __launch_bounds__(160, 2)
+//
+// FP = 2: two frames per pass.  Consumer warps w and w + 4 own the same pixel
+// pairs (the same TMEM lane quarter, so they share one delay table) but
+// accumulate different frames; each TMA box carries both frames' windows
+// ({W, G, 2}).  Twice the warps per SM for the same TMEM, so twice the
+// independent instruction streams to hide the FP32 / shared-memory latencies.
+template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false, int FP = 1>
+__global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
   using O = R<float>;
   using L = Lane<true>;
   typedef u64 VT;
-  constexpr int NTH = 160, NC = 128;  // threads, consumer threads
+  constexpr int NTH = 32 * (4 * FP + 1), NC = 128;  // threads, pixel-pair threads
+  constexpr int NCW = 4 * FP;                        // consumer warps
   constexpr int TZk = 16, TXk = 16;
   constexpr int G = IDMAP ? 4 : 1;  // receive channels per TMA box (rows of W samples)
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx;
   const int W = a.W, nst = a.nst;
-  const TmaLayout lay(n_tx, n_el, TJC, nst, W, PW);
+  const TmaLayout lay(n_tx, n_el, TJC, nst, W, PW, FP);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
@@ -124,14 +131,16 @@ __global__ void __launch_bounds__(160, 2)
   int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
   float* rmin = reinterpret_cast<float*>(smem_raw + lay.rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
-  int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][TJC] gather base K
+  int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][FP][TJC] gather base K
   int* metaM = reinterpret_cast<int*>(smem_raw + lay.metaM);    // [nst][TJC] element m
   u64* txd_s = reinterpret_cast<u64*>(smem_raw + lay.txd);      // PW: [n_tx][128]
-  const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC][W] f32
+  const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC/G][FP][G][W] f32
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const bool producer = warp == 4;
+  const bool producer = warp == NCW;
+  const int slot = (warp >> 2) & (FP - 1);  // consumer: frame slot of the pass
+  const int ctid = tid & (NC - 1);          // consumer: pixel-pair thread index
   const int tiles_x = (g.n_x + TXk - 1) / TXk;
   const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TXk;
   const int col = tx0 + (warp & 1) * 8 + (lane & 7);
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(160, 2)
   if (producer && lane == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(full_s + 8 * s, 32);  // the producer's 32 lanes (one carries expect_tx)
-      mbar_init(empty_s + 8 * s, 4);  // one arrival per consumer warp
+      mbar_init(empty_s + 8 * s, NCW);  // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rf_map)) : "memory");
@@ -166,7 +175,8 @@ __global__ void __launch_bounds__(160, 2)
 
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
   if (!producer) {
-    for (int m = 0; m < n_el; ++m) {
+    // the FP warps sharing a lane quarter split the elements
+    for (int m = slot; m < n_el; m += FP) {
       const float dx = O::from_double(g.elem_x[m] - px);
       const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
       const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(160, 2)
       };
       const float* hA = row(i0A, i1A);
       const float* hB = row(i0B, i1B);
-      for (int m = 0; m < n_el; ++m) {
+      for (int m = slot; m < n_el; m += FP) {
         const float wA = (m >= i0A && m <= i1A) ? (hA ? hA[m - i0A] : 1.0f) : 0.0f;
         const float wB = (m >= i0B && m <= i1B) ? (hB ? hB[m - i0B] : 1.0f) : 0.0f;
         tm_st2(tlane + 2 * n_el + 2 * m, wA, wB);
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(160, 2)
       rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
     }
   }
-  if (PW && !producer) {
+  if (PW && !producer && slot == 0) {
     // exact transmit delays fs*((z cos + x sin)/c) of the pixel pair for every
     // angle (beamform.py:218-225), once per CTA
     for (int e = 0; e < n_tx; ++e) {
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(160, 2)
       const float xs = O::mul(pxd, sa);
       const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
       const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
-      txd_s[e * NC + tid] = pk(tA, tB);
+      txd_s[e * NC + ctid] = pk(tA, tB);
     }
   }
   __syncthreads();
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(160, 2)
   const int n_chunks = (n_rx + TJC - 1) / TJC;
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
-  const int Q = f_count * n_tx * n_chunks;
+  const int Q = ((f_count + FP - 1) / FP) * n_tx * n_chunks;  // passes x transmits x stages
 
   if (producer) {
     // ================= producer warp: window starts + TMA issue
@@ -260,7 +270,7 @@ __global__ void __launch_bounds__(160, 2)
       const int jb = cu.cb * TJC;
       const int jn = min(TJC, n_rx - jb);
       const int row0 = e * n_rx + jb;
-      const int fr = f_begin + cu.fl;
+      const int fr = f_begin + cu.fl * FP;  // first frame of the pass
       const uint32_t bar = full_s + 8 * s;
       const int ngr = (jn + G - 1) / G;  // boxes this chunk
 #pragma unroll
@@ -280,20 +290,25 @@ __global__ void __launch_bounds__(160, 2)
             metaM[s * TJC + jj0] = m;
           }
           const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
-          const uint32_t dst = win_s + (uint32_t)((s * TJC + jj0) * W) * 4u;
-          const uint32_t K0 = dst - (uint32_t)(kMagicBits + ws) * 4u;
-          if (G == 4) {
-            const uint32_t rs = (uint32_t)W * 4u;
-            *reinterpret_cast<int4*>(metaK + s * TJC + jj0) =
-                make_int4((int)K0, (int)(K0 + rs), (int)(K0 + 2 * rs), (int)(K0 + 3 * rs));
-          } else {
-            metaK[s * TJC + jj0] = (int)K0;
+          // box = [FP frames][G traces][W samples]
+          const uint32_t dst = win_s + (uint32_t)((s * TJC + jj0) * FP * W) * 4u;
+#pragma unroll
+          for (int f = 0; f < FP; ++f) {
+            const uint32_t K0 = dst + (uint32_t)(f * G * W) * 4u - (uint32_t)(kMagicBits + ws) * 4u;
+            int* mk = metaK + (s * FP + f) * TJC + jj0;
+            if (G == 4) {
+              const uint32_t rs = (uint32_t)W * 4u;
+              *reinterpret_cast<int4*>(mk) =
+                  make_int4((int)K0, (int)(K0 + rs), (int)(K0 + 2 * rs), (int)(K0 + 3 * rs));
+            } else {
+              *mk = (int)K0;
+            }
           }
           tma_load_3d(dst, &rf_map, ws, row0 + jj0, fr, bar);
         }
       }
       if (lane == 0)
-        mbar_arrive_tx(bar, (uint32_t)(ngr * G * W * 4));
+        mbar_arrive_tx(bar, (uint32_t)(ngr * G * FP * W * 4));
       else
         mbar_arrive(bar);
       cu.next(n_chunks, n_tx);
@@ -315,12 +330,12 @@ __global__ void __launch_bounds__(160, 2)
       mbar_wait(full_s + 8 * s, ph);
       if (cur.cb == 0) {
         if (PW)
-          txd = (VT)txd_s[cur.e * NC + tid];
+          txd = (VT)txd_s[cur.e * NC + ctid];
         else
           txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
         t0e2 = L::splat(t0v[cur.e]);
       }
-      const int* MKc = metaK + s * TJC;
+      const int* MKc = metaK + (s * FP + slot) * TJC;
       const int* MMc = metaM + s * TJC;
       const int4* MK4 = reinterpret_cast<const int4*>(MKc);  // 4 gather bases per LDS.128
       const int jn = min(TJC, n_rx - cur.cb * TJC);
@@ -393,8 +408,9 @@ __global__ void __launch_bounds__(160, 2)
       if (lane == 0) mbar_arrive(empty_s + 8 * s);  // stage s may be refilled
 
       if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
-        const int64_t fo = (int64_t)(f_begin + cur.fl) * a.out_stride;
-        if (col < g.n_x) {
+        const int fl = cur.fl * FP + slot;  // this warp's frame in the CTA's group
+        const int64_t fo = (int64_t)(f_begin + fl) * a.out_stride;
+        if (col < g.n_x && fl < f_count) {
           float oA, oB;
           unpk((u64)acc, oA, oB);
           if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
@@ -461,7 +477,8 @@ static bool tma_has128(const bm_das_geometry& g) {
 }
 
 // channels per stage and stage count for the shared-memory share of one CTA
-static bool tma_plan(const bm_das_geometry& g, int& tjc, int& nst, size_t& smem) {
+// (fp frames per pass: every stage holds fp frames' windows)
+static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_t& smem) {
   const int W = tma_window(g);
   const int per_sm = 512 / tma_cols(g);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
@@ -470,11 +487,11 @@ static bool tma_plan(const bm_das_geometry& g, int& tjc, int& nst, size_t& smem)
   const int only = ev ? atoi(ev) : 0;
   for (int t : {128, 64, 32}) {
     if (t > g.n_rx && t > 32) continue;
-    if (t == 128 && !tma_has128(g)) continue;
+    if (t == 128 && (!tma_has128(g) || fp != 1)) continue;
     if (only && t != only) continue;
     int n = kTmaMaxStages;
-    while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw).total > cap) --n;
-    if (n >= (t == 64 ? 3 : 2)) {
+    while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw, fp).total > cap) --n;
+    if (n >= (t == 64 && fp == 1 ? 3 : 2)) {
       tjc = t;
       nst = n;
       smem = cap;
@@ -493,7 +510,7 @@ int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if ((int64_t)g.n_tx * g.n_rx > 0x7fffffffLL) return 0;
   int tjc, nst;
   size_t smem;
-  if (!tma_plan(g, tjc, nst, smem)) return 0;
+  if (!tma_plan(g, 1, tjc, nst, smem)) return 0;
   return encode_tiled() != nullptr;
 }
 
@@ -502,29 +519,45 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   if (((uintptr_t)rf & 15) != 0) return -1;  // caller falls back
   int tjc, nst;
   size_t smem;
-  if (!tma_plan(g, tjc, nst, smem)) return -1;
+  if (!tma_plan(g, 1, tjc, nst, smem)) return -1;
   const int W = tma_window(g);
+  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
+  const int per_sm = 512 / tma_cols(g);
+  // frames per CTA: amortise the per-CTA delay-table build over a frame
+  // group while keeping >= 4 waves of CTAs for load balance
+  int fpc = 1;
+  while (fpc < 16 && fpc * 2 <= n_frames &&
+         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
+    fpc *= 2;
+  // two frames per pass (8 consumer warps sharing one delay table) for
+  // identity-map apertures whenever a CTA owns >= 2 frames
+  int fp = 1;
+  {
+    const char* e = getenv("BM_DAS_FP");  // tuning override: 1 | 2
+    const int want = e ? atoi(e) : 2;
+    int t2, n2;
+    size_t s2;
+    if (want == 2 && g.rx_identity && fpc >= 2 && tma_plan(g, 2, t2, n2, s2)) {
+      fp = 2;
+      tjc = t2;
+      nst = n2;
+      smem = s2;
+    }
+  }
   // RF as a 3-D tensor: samples x (transmit, channel) rows x frames
   CUtensorMap map;
   const int64_t fstride = n_frames > 1 ? rf_stride : (int64_t)g.n_tx * g.n_rx * g.n_samples;
   cuuint64_t dims[3] = {(cuuint64_t)g.n_samples, (cuuint64_t)g.n_tx * g.n_rx,
                         (cuuint64_t)n_frames};
   cuuint64_t strides[2] = {(cuuint64_t)g.n_samples * 4, (cuuint64_t)fstride * 4};
-  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, 1};
+  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, (cuuint32_t)fp};
   cuuint32_t estr[3] = {1, 1, 1};
   if (encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(rf), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
-  const int per_sm = 512 / tma_cols(g);
-  TmaArgs a{g, (float*)out, out_stride, n_frames, 1, W, nst, tma_cols(g)};
-  int fpc = 1;
-  while (fpc < 16 && fpc * 2 <= n_frames &&
-         (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
-    fpc *= 2;
-  a.frames_per_cta = fpc;
+  TmaArgs a{g, (float*)out, out_stride, n_frames, fpc, W, nst, tma_cols(g)};
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
 #define BM_TMA_ROW(J, WT)                                                                  \
@@ -553,11 +586,28 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     if (!tma_has128(g)) return -1;
     k = pw ? das_tma_kernel<true, true, false, true, 128> : das_tma_kernel<false, true, false, true, 128>;
   }
+  if (fp == 2) {
+#define BM_TMA_FP2(J, WT)                                                                   \
+  das_tma_kernel<false, false, false, true, J, WT, 2>,                                      \
+      das_tma_kernel<false, false, true, true, J, WT, 2>,                                   \
+      das_tma_kernel<false, true, false, true, J, WT, 2>,                                   \
+      das_tma_kernel<false, true, true, true, J, WT, 2>,                                    \
+      das_tma_kernel<true, false, false, true, J, WT, 2>,                                   \
+      das_tma_kernel<true, false, true, true, J, WT, 2>,                                    \
+      das_tma_kernel<true, true, false, true, J, WT, 2>,                                    \
+      das_tma_kernel<true, true, true, true, J, WT, 2>
+    // identity map only; rows: uniform/32, uniform/64, weighted/32, weighted/64
+    static const kfn table2[32] = {BM_TMA_FP2(32, false), BM_TMA_FP2(64, false),
+                                   BM_TMA_FP2(32, true), BM_TMA_FP2(64, true)};
+#undef BM_TMA_FP2
+    k = table2[(g.uniform ? 0 : 16) + (tjc >= 64 ? 8 : 0) +
+               ((pw ? 4 : 0) | (lin ? 2 : 0) | (g.t0_nonzero ? 1 : 0))];
+  }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
-  k<<<grid, 160, smem, s>>>(map, a);
+  k<<<grid, 32 * (4 * fp + 1), smem, s>>>(map, a);
   return cuda_status();
 }
 

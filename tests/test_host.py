@@ -158,7 +158,8 @@ def test_no_contracted_fma_in_das_kernels():
     # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch, tma-32ch, tma-64ch,
     # weighted tma-32ch, weighted tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0}
     # x {identity map, general} + 2 tma-128ch (uniform linear identity-map, STA | PW)
-    assert len(das) == 146
+    # + 32 two-frames-per-pass tma (identity map) x {32, 64}ch x {uniform, weighted}
+    assert len(das) == 178
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
