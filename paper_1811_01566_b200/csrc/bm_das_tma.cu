@@ -78,7 +78,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // spinning producer warp issued ~9 % of all instructions of the kernel
 // (SYNCS.PHASECHK + BRA), on an SMSP that it shares with consumers.
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) __nanosleep(100);
+  while (!mbar_try(bar, parity)) __nanosleep(32);
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -529,6 +529,10 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   while (fpc < 16 && fpc * 2 <= n_frames &&
          (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
     fpc *= 2;
+  if (const char* e = getenv("BM_DAS_FPC")) {  // test hook: force the frames per CTA
+    const int want = atoi(e);
+    if (want >= 1) fpc = want < n_frames ? want : n_frames;
+  }
   // two frames per pass (8 consumer warps sharing one delay table) for
   // identity-map apertures whenever a CTA owns >= 2 frames
   int fp = 1;
