@@ -333,9 +333,19 @@ __global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restri
     tw[m] = make_float2((float)cs, (float)sn);
   }
   const float* xo = x + o * (int64_t)N * inner + i_base;
-  for (int idx = tid; idx < N * L; idx += 256) {
-    const int l = idx & (L - 1), k = idx >> 3;
-    tile[k * LP + l] = l < lanes ? xo[(int64_t)k * inner + l] : 0.0f;
+  {
+    // all R loads of a thread in flight before the first shared-memory store
+    float ld[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int idx = tid + 256 * q, l = idx & (L - 1), k = idx >> 3;
+      ld[q] = l < lanes ? __ldg(xo + (int64_t)k * inner + l) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int idx = tid + 256 * q;
+      tile[(idx >> 3) * LP + (idx & (L - 1))] = ld[q];
+    }
   }
   __syncthreads();
 
