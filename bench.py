@@ -347,7 +347,12 @@ def main():
     #  * shared-memory gathers: 2 x 4 B per linear contribution (1 nearest);
     #    LDS.32 retires 1 warp-instr/clk/SM = 128 B/clk/SM.
     # The binding roof is the slower of the two; HBM is ~100x away.
-    ops = 9 if args.interp == "linear" else 4
+    #  * a thread that accumulates ft frames (bm_das_launch_shape) computes the
+    #    frame-independent part once per (pixel, channel): linear 5 lane-ops
+    #    (t, floor, k0, a, 1-a) + 4 per frame, nearest 3 (t, +0.5, floor) + 1.
+    shape = eng.plan.launch_shape(n_s, B, args.interp) or {"ft": 1}
+    ft = shape["ft"]
+    ops = (5.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 1.0)
     gb = 8 if args.interp == "linear" else 4
     t_fp32 = contrib * ops / (n_sm * 128 * sm_mhz * 1e6)
     t_lds = contrib * gb / (n_sm * 128 * sm_mhz * 1e6)
@@ -358,10 +363,13 @@ def main():
         "kernel_ms_per_launch": round(das_ms, 4),
         "algorithmic_bytes_per_launch": das_bytes,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-        "note": "DAS is FP32-pipe bound, not HBM bound: see binding",
+        "note": "DAS is bound on chip (SMEM gathers / FP32 pipe), not by HBM: see binding",
         "binding": {
-            "resource": ("FP32 pipe (9 lane-ops per linear contribution, 128 lane-ops/clk/SM); "
-                         "SMEM gather roof (8 B per contribution, 128 B/clk/SM) reported beside"),
+            "resource": ("max of: SMEM gather roof (%d B per contribution, 128 B/clk/SM) and "
+                         "FP32 pipe (%.4g lane-ops per contribution at %d frame(s) per thread, "
+                         "128 lane-ops/clk/SM)" % (gb, ops, ft)),
+            "bound_by": "smem_gather" if t_lds >= t_fp32 else "fp32",
+            "launch_shape": shape,
             "contributions_per_launch": contrib,
             "achieved_gcontrib_s": round(contrib / (das_ms / 1000.0) / 1e9, 1),
             "achieved_tflops_fp32_lane_ops": round(contrib * ops / (das_ms / 1000.0) / 1e12, 2),
@@ -376,7 +384,7 @@ def main():
     if not args.no_cpu and args.cpu_seconds > 0:
         fps, cores, n, el = cpu_reference(ctx, grid, host[:4], args.cpu_seconds, args.interp)
         cpu = {"value": round(fps, 4), "unit": "frames/s", "cores": cores, "kind": "port",
-               "sample": f"{n} cfg2 frames in {el:.1f}s: oracle/ C DAS (pthreads) + scipy.fft "
+               "sample": f"{n} {args.config} frames in {el:.1f}s: oracle/ C DAS (pthreads) + scipy.fft "
                          f"+ numpy dB, plan prebuilt"}
 
     line = {

@@ -124,6 +124,14 @@ int bm_das_prepare(bm_das_geometry* g, const double* elem_x_host, const double* 
  * (scalar / pixel pair / hybrid), -1 invalid geometry.  Host only. */
 int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride);
 
+/* Launch shape of the TMA kernel (bm_das_select == 5) for n_frames frames:
+ * shape[6] = {frames per CTA, FP consumer warp groups sharing one TMEM delay
+ * table, FT frames per thread, receive channels per pipeline stage, stages,
+ * samples per staged window}.  A pass covers FP * FT frames.  Returns 0, or
+ * -1 when another kernel would run.  Host only. */
+int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_stride, int32_t n_frames,
+                        int32_t* shape);
+
 /* Delay-and-Sum of n_frames frames.
  *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride
  *   out: device dtype[n_frames][n_z][n_x],  frame f at out + f*out_frame_stride

@@ -47,6 +47,7 @@ SIGNATURES = {
     "bm_das_aperture_span": ([ctypes.POINTER(DasGeometry), _D, _P, _P], ctypes.c_int),
     "bm_das_prepare": ([ctypes.POINTER(DasGeometry), _P, _P, _P, _P, _P], ctypes.c_int),
     "bm_das_select": ([ctypes.POINTER(DasGeometry), _I64], ctypes.c_int),
+    "bm_das_launch_shape": ([ctypes.POINTER(DasGeometry), _I64, _I32, _P], ctypes.c_int),
     "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
     "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P], ctypes.c_int),
     "bm_envelope": ([_I32, _P, _P, _I64, _P], ctypes.c_int),

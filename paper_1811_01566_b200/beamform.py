@@ -178,6 +178,19 @@ class DasPlan:
         stride = int(self._geom.n_tx) * int(self.n_rx) * int(n_samples)
         return self.KERNELS.get(N.load().bm_das_select(ctypes.byref(g), stride), "invalid")
 
+    def launch_shape(self, n_samples: int, n_frames: int, interp: str = "linear") -> dict | None:
+        """Launch shape of the TMA kernel for a batch of ``n_frames`` frames
+        (``bm_das_launch_shape``), or None when another kernel would run.
+        ``fp * ft`` frames share one pass: ``fp`` consumer warp groups read
+        one TMEM delay table, each thread accumulates ``ft`` frames."""
+        g = self.geometry(n_samples, interp, True)
+        stride = int(self._geom.n_tx) * int(self.n_rx) * int(n_samples)
+        shape = (ctypes.c_int32 * 6)()
+        if N.load().bm_das_launch_shape(ctypes.byref(g), stride, int(n_frames), shape) != 0:
+            return None
+        return dict(zip(("frames_per_cta", "fp", "ft", "channels_per_stage", "stages",
+                         "window"), list(shape)))
+
     def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True):
         """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
         ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``."""

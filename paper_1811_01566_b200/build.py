@@ -8,6 +8,7 @@ snapshot to the GPU box.
 
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -53,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "_lib", "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    jobs = []
     for src in sources():
         name = os.path.basename(src)
         obj = os.path.join(objdir, name + ".o")
@@ -64,8 +65,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        jobs.append((obj, cmd))
+    # one nvcc per translation unit, in parallel
+    with concurrent.futures.ThreadPoolExecutor(max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for _ in ex.map(lambda j: subprocess.run(j[1], check=True), jobs):
+            pass
+    objs = [o for o, _ in jobs]
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp",
            *objs]
     subprocess.run(cmd, check=True)

@@ -58,6 +58,7 @@ int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
                     int64_t out_stride, int n_frames, cudaStream_t s);
 int das_tmem_variant(const bm_das_geometry& g);
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride);
+int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);
 // returns -1 when this launch cannot use the TMA kernel (caller falls back)
 int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                    int64_t out_stride, int n_frames, cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid

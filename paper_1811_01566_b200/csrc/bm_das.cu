@@ -243,6 +243,15 @@ extern "C" int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride) 
   return 0;
 }
 
+extern "C" int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_stride,
+                                   int32_t n_frames, int32_t* shape) {
+  if (!shape || bm::check_geometry(g)) return -1;
+  const int choice = bm::das_kernel_choice();
+  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride))
+    return bm::das_tma_shape(*g, n_frames, shape);
+  return -1;
+}
+
 extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
                                void* out, int64_t out_frame_stride, int32_t n_frames,
                                void* stream) {

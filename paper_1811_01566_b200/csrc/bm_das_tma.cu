@@ -23,6 +23,7 @@
 // (row l/8 + 4, col l%8) of its warp's 8 x 8 block, TMEM lane 32w + l holds
 // the pair's delays to element m in columns 2m, 2m+1.
 #include <cuda.h>  // CUtensorMap
+#include <stdio.h>
 
 #include "bm_tmem.cuh"
 
@@ -106,7 +107,16 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // accumulate different frames; each TMA box carries both frames' windows
 // ({W, G, 2}).  Twice the warps per SM for the same TMEM, so twice the
 // independent instruction streams to hide the FP32 / shared-memory latencies.
-template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false, int FP = 1>
+//
+// FT = 2: two frames per THREAD.  The delay t, the sample index, a and 1 - a
+// of a (pixel, channel) do not depend on the frame, so a thread that
+// accumulates two frames computes them once: 13 FP32 instructions per pixel
+// pair, channel and two frames instead of 18, and the per-frame gathers of
+// the second frame reuse the first frame's addresses plus the frame-plane
+// offset of the staged box.  A pass then covers FP * FT frames (box
+// {W, G, FP * FT}); each accumulator keeps the reference's e -> j order.
+template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false, int FP = 1,
+          int FT = 1>
 __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
   using O = R<float>;
@@ -114,12 +124,13 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   typedef u64 VT;
   constexpr int NTH = 32 * (4 * FP + 1), NC = 128;  // threads, pixel-pair threads
   constexpr int NCW = 4 * FP;                        // consumer warps
+  constexpr int FPP = FP * FT;                       // frames per pass
   constexpr int TZk = 16, TXk = 16;
   constexpr int G = IDMAP ? 4 : 1;  // receive channels per TMA box (rows of W samples)
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx;
   const int W = a.W, nst = a.nst;
-  const TmaLayout lay(n_tx, n_el, TJC, nst, W, PW, FP);
+  const TmaLayout lay(n_tx, n_el, TJC, nst, W, PW, FPP);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
@@ -131,10 +142,10 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
   float* rmin = reinterpret_cast<float*>(smem_raw + lay.rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
-  int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][FP][TJC] gather base K
+  int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][FPP][TJC] gather base K
   int* metaM = reinterpret_cast<int*>(smem_raw + lay.metaM);    // [nst][TJC] element m
   u64* txd_s = reinterpret_cast<u64*>(smem_raw + lay.txd);      // PW: [n_tx][128]
-  const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC/G][FP][G][W] f32
+  const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC/G][FPP][G][W] f32
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   const int n_chunks = (n_rx + TJC - 1) / TJC;
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
-  const int Q = ((f_count + FP - 1) / FP) * n_tx * n_chunks;  // passes x transmits x stages
+  const int Q = ((f_count + FPP - 1) / FPP) * n_tx * n_chunks;  // passes x transmits x stages
 
   if (producer) {
     // ================= producer warp: window starts + TMA issue
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       const int jb = cu.cb * TJC;
       const int jn = min(TJC, n_rx - jb);
       const int row0 = e * n_rx + jb;
-      const int fr = f_begin + cu.fl * FP;  // first frame of the pass
+      const int fr = f_begin + cu.fl * FPP;  // first frame of the pass
       const uint32_t bar = full_s + 8 * s;
       const int ngr = (jn + G - 1) / G;  // boxes this chunk
 #pragma unroll
@@ -290,12 +301,12 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
             metaM[s * TJC + jj0] = m;
           }
           const int ws = ((int)floorf(lo_e + rlo) - 3) & ~3;
-          // box = [FP frames][G traces][W samples]
-          const uint32_t dst = win_s + (uint32_t)((s * TJC + jj0) * FP * W) * 4u;
+          // box = [FPP frames][G traces][W samples]
+          const uint32_t dst = win_s + (uint32_t)((s * TJC + jj0) * FPP * W) * 4u;
 #pragma unroll
-          for (int f = 0; f < FP; ++f) {
+          for (int f = 0; f < FPP; ++f) {
             const uint32_t K0 = dst + (uint32_t)(f * G * W) * 4u - (uint32_t)(kMagicBits + ws) * 4u;
-            int* mk = metaK + (s * FP + f) * TJC + jj0;
+            int* mk = metaK + (s * FPP + f) * TJC + jj0;
             if (G == 4) {
               const uint32_t rs = (uint32_t)W * 4u;
               *reinterpret_cast<int4*>(mk) =
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         }
       }
       if (lane == 0)
-        mbar_arrive_tx(bar, (uint32_t)(ngr * G * FP * W * 4));
+        mbar_arrive_tx(bar, (uint32_t)(ngr * G * FPP * W * 4));
       else
         mbar_arrive(bar);
       cu.next(n_chunks, n_tx);
@@ -321,8 +332,12 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     // ================= consumer warps: gather + interpolate + accumulate
     const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
     const VT ONE2 = L::splat(1.0f), HALF2 = L::splat(0.5f);
-    VT acc = L::splat(0.0f);  // +0.0f
-    VT txd = acc, t0e2 = acc;
+    VT acc[FT];
+#pragma unroll
+    for (int i = 0; i < FT; ++i) acc[i] = L::splat(0.0f);  // +0.0f
+    VT txd = acc[0], t0e2 = acc[0];
+    // the thread's frame i > 0 sits i frame planes ({G, W} floats) after frame 0
+    const uint32_t FOFF = (uint32_t)(G * W) * 4u;
     Cursor cur{0, 0, 0, 0};
     int s = 0;
     uint32_t ph = 0;
@@ -335,7 +350,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
           txd = (VT)tm_ld2(tlane + 2 * txe[cur.e]);
         t0e2 = L::splat(t0v[cur.e]);
       }
-      const int* MKc = metaK + (s * FP + slot) * TJC;
+      const int* MKc = metaK + (s * FPP + slot * FT) * TJC;
       const int* MMc = metaM + s * TJC;
       const int4* MK4 = reinterpret_cast<const int4*>(MKc);  // 4 gather bases per LDS.128
       const int jn = min(TJC, n_rx - cur.cb * TJC);
@@ -350,20 +365,27 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         const uint32_t aA = (uint32_t)__float_as_int(rA) * 4u + K;
         const uint32_t aB = (uint32_t)__float_as_int(rB) * 4u + K;
         if (LINEAR) {
-          const VT x0 = L::make(lds0(aA), lds0(aB));
-          const VT x1 = L::make(lds1(aA), lds1(aB));
           const VT fr = L::sub(t, L::add(r, NM2));  // a = t - floor(t)
           const VT om = L::sub(ONE2, fr);           // 1 - a
+          VT wom = om, wfr = fr;
           if (WT) {
-            acc = L::add(acc, L::mul(L::mul(wgt, om), x0));  // out + (w*(1-a)) * x[k0]
-            acc = L::add(acc, L::mul(L::mul(wgt, fr), x1));  // acc + (w*a) * x[k1]
-          } else {
-            acc = L::add(acc, L::mul(om, x0));  // acc = out + (1 - a) * x[k0]
-            acc = L::add(acc, L::mul(fr, x1));  // out = acc + a * x[k1]
+            wom = L::mul(wgt, om);  // w * (1 - a)
+            wfr = L::mul(wgt, fr);  // w * a
+          }
+#pragma unroll
+          for (int i = 0; i < FT; ++i) {
+            const uint32_t fA = aA + i * FOFF, fB = aB + i * FOFF;
+            const VT x0 = L::make(lds0(fA), lds0(fB));
+            const VT x1 = L::make(lds1(fA), lds1(fB));
+            acc[i] = L::add(acc[i], L::mul(wom, x0));  // acc = out + (w*(1-a)) * x[k0]
+            acc[i] = L::add(acc[i], L::mul(wfr, x1));  // out = acc + (w*a) * x[k1]
           }
         } else {
-          const VT x = L::make(lds0(aA), lds0(aB));
-          acc = L::add(acc, WT ? L::mul(wgt, x) : x);
+#pragma unroll
+          for (int i = 0; i < FT; ++i) {
+            const VT x = L::make(lds0(aA + i * FOFF), lds0(aB + i * FOFF));
+            acc[i] = L::add(acc[i], WT ? L::mul(wgt, x) : x);
+          }
         }
       };
       if (IDMAP && jn == TJC) {
@@ -403,20 +425,24 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       }
       // every gathered sample feeds acc: pinning acc before the arrive keeps
       // the (non-volatile) shared loads of this stage ahead of its release
-      asm volatile("" ::"l"(acc));
+#pragma unroll
+      for (int i = 0; i < FT; ++i) asm volatile("" ::"l"(acc[i]));
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_s + 8 * s);  // stage s may be refilled
 
       if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
-        const int fl = cur.fl * FP + slot;  // this warp's frame in the CTA's group
-        const int64_t fo = (int64_t)(f_begin + fl) * a.out_stride;
-        if (col < g.n_x && fl < f_count) {
-          float oA, oB;
-          unpk((u64)acc, oA, oB);
-          if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
-          if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = oB;
+#pragma unroll
+        for (int i = 0; i < FT; ++i) {
+          const int fl = cur.fl * FPP + slot * FT + i;  // this thread's frame in the CTA's group
+          const int64_t fo = (int64_t)(f_begin + fl) * a.out_stride;
+          if (col < g.n_x && fl < f_count) {
+            float oA, oB;
+            unpk((u64)acc[i], oA, oB);
+            if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
+            if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = oB;
+          }
+          acc[i] = L::splat(0.0f);
         }
-        acc = L::splat(0.0f);
       }
       cur.next(n_chunks, n_tx);
       if (++s == nst) {
@@ -479,15 +505,17 @@ static bool tma_has128(const bm_das_geometry& g) {
 // channels per stage and stage count for the shared-memory share of one CTA
 // (fp frames per pass: every stage holds fp frames' windows)
 static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_t& smem) {
+  if (fp > 4) return false;
   const int W = tma_window(g);
   const int per_sm = 512 / tma_cols(g);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   const bool pw = g.scheme == BM_PW;
   const char* ev = getenv("BM_DAS_TJC");  // tuning override: 32 | 64 | 128
   const int only = ev ? atoi(ev) : 0;
-  for (int t : {128, 64, 32}) {
+  for (int t : {128, 64, 32, 16}) {
     if (t > g.n_rx && t > 32) continue;
     if (t == 128 && (!tma_has128(g) || fp != 1)) continue;
+    if (t == 16 && fp < 4) continue;  // 16-channel stages: four frames per pass only
     if (only && t != only) continue;
     int n = kTmaMaxStages;
     while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw, fp).total > cap) --n;
@@ -514,13 +542,15 @@ int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   return encode_tiled() != nullptr;
 }
 
-int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
-                   int64_t out_stride, int n_frames, cudaStream_t s) {
-  if (((uintptr_t)rf & 15) != 0) return -1;  // caller falls back
-  int tjc, nst;
+// Launch shape of a TMA DAS launch over n_frames frames: frames per CTA, the
+// pass shape (fp warp groups sharing one delay table x ft frames per thread)
+// and the stage plan.  False when the TMA kernel cannot run this geometry.
+struct TmaChoice {
+  int fpc, fp, ft, tjc, nst;
   size_t smem;
-  if (!tma_plan(g, 1, tjc, nst, smem)) return -1;
-  const int W = tma_window(g);
+};
+static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
+  if (!tma_plan(g, 1, c.tjc, c.nst, c.smem)) return false;
   const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
   const int per_sm = 512 / tma_cols(g);
   // frames per CTA: amortise the per-CTA delay-table build over a frame
@@ -533,28 +563,63 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     const int want = atoi(e);
     if (want >= 1) fpc = want < n_frames ? want : n_frames;
   }
-  // two frames per pass (8 consumer warps sharing one delay table) for
-  // identity-map apertures whenever a CTA owns >= 2 frames
-  int fp = 1;
-  {
+  c.fpc = fpc;
+  // several frames per pass for identity-map apertures whenever a CTA owns
+  // enough frames: fp consumer warp groups share one delay table (FP), each
+  // thread accumulates ft frames (FT)
+  c.fp = c.ft = 1;
+  if (g.rx_identity) {
     const char* e = getenv("BM_DAS_FP");  // tuning override: 1 | 2
-    const int want = e ? atoi(e) : 2;
-    int t2, n2;
-    size_t s2;
-    if (want == 2 && g.rx_identity && fpc >= 2 && tma_plan(g, 2, t2, n2, s2)) {
-      fp = 2;
-      tjc = t2;
-      nst = n2;
-      smem = s2;
+    const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2
+    const int want_fp = e ? atoi(e) : 2, want_ft = e2 ? atoi(e2) : 2;
+    const bool ft2_ok = g.uniform && !g.t0_nonzero;
+    const int cand[3][2] = {{want_fp, want_ft}, {1, want_ft}, {want_fp, 1}};
+    for (const auto& cd : cand) {
+      const int f = cd[0] == 2 ? 2 : 1, t = cd[1] == 2 ? 2 : 1;
+      if (f * t == 1 || (t == 2 && !ft2_ok) || fpc < f * t) continue;
+      int t2, n2;
+      size_t s2;
+      if (tma_plan(g, f * t, t2, n2, s2)) {
+        c.fp = f;
+        c.ft = t;
+        c.tjc = t2;
+        c.nst = n2;
+        c.smem = s2;
+        break;
+      }
     }
   }
+  return true;
+}
+
+int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape) {
+  TmaChoice c;
+  if (n_frames < 1 || !tma_choose(g, n_frames, c)) return -1;
+  shape[0] = c.fpc;
+  shape[1] = c.fp;
+  shape[2] = c.ft;
+  shape[3] = c.tjc;
+  shape[4] = c.nst;
+  shape[5] = tma_window(g);
+  return 0;
+}
+
+int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                   int64_t out_stride, int n_frames, cudaStream_t s) {
+  if (((uintptr_t)rf & 15) != 0) return -1;  // caller falls back
+  TmaChoice c;
+  if (!tma_choose(g, n_frames, c)) return -1;
+  const int W = tma_window(g);
+  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
+  const int fpc = c.fpc, fp = c.fp, ft = c.ft, tjc = c.tjc, nst = c.nst;
+  const size_t smem = c.smem;
   // RF as a 3-D tensor: samples x (transmit, channel) rows x frames
   CUtensorMap map;
   const int64_t fstride = n_frames > 1 ? rf_stride : (int64_t)g.n_tx * g.n_rx * g.n_samples;
   cuuint64_t dims[3] = {(cuuint64_t)g.n_samples, (cuuint64_t)g.n_tx * g.n_rx,
                         (cuuint64_t)n_frames};
   cuuint64_t strides[2] = {(cuuint64_t)g.n_samples * 4, (cuuint64_t)fstride * 4};
-  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, (cuuint32_t)fp};
+  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, (cuuint32_t)(fp * ft)};
   cuuint32_t estr[3] = {1, 1, 1};
   if (encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(rf), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -607,10 +672,30 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     k = table2[(g.uniform ? 0 : 16) + (tjc >= 64 ? 8 : 0) +
                ((pw ? 4 : 0) | (lin ? 2 : 0) | (g.t0_nonzero ? 1 : 0))];
   }
+  if (ft == 2) {
+    // uniform identity-map no-t0 apertures (the BASELINE configurations),
+    // linear and nearest; rows: FP = 1 / 2 x 16 / 32 / 64-channel stages (16
+    // only with four frames per pass)
+#define BM_TMA_FT2(J, F)                                                                   \
+  das_tma_kernel<false, false, false, true, J, false, F, 2>,                               \
+      das_tma_kernel<true, false, false, true, J, false, F, 2>,                            \
+      das_tma_kernel<false, true, false, true, J, false, F, 2>,                            \
+      das_tma_kernel<true, true, false, true, J, false, F, 2>
+    static const kfn table3[24] = {nullptr,           nullptr, nullptr, nullptr,
+                                   BM_TMA_FT2(32, 1), BM_TMA_FT2(64, 1),
+                                   BM_TMA_FT2(16, 2), BM_TMA_FT2(32, 2), BM_TMA_FT2(64, 2)};
+#undef BM_TMA_FT2
+    if (tjc > 64) return -1;
+    k = table3[(fp == 2 ? 12 : 0) + (tjc == 64 ? 8 : tjc == 32 ? 4 : 0) + (lin ? 2 : 0) +
+               (pw ? 1 : 0)];
+    if (!k) return -1;
+  }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
+  if (const char* e = getenv("BM_DAS_VERBOSE"))
+    if (atoi(e)) fprintf(stderr, "das_tma: fp=%d ft=%d tjc=%d nst=%d W=%d fpc=%d smem=%zu\n", fp, ft, tjc, nst, W, fpc, smem);
   k<<<grid, 32 * (4 * fp + 1), smem, s>>>(map, a);
   return cuda_status();
 }

@@ -159,7 +159,9 @@ def test_no_contracted_fma_in_das_kernels():
     # weighted tma-32ch, weighted tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0}
     # x {identity map, general} + 2 tma-128ch (uniform linear identity-map, STA | PW)
     # + 32 two-frames-per-pass tma (identity map) x {32, 64}ch x {uniform, weighted}
-    assert len(das) == 178
+    # + 20 two-frames-per-thread tma (uniform identity map, no t0) x {STA, PW} x
+    # {nearest, linear}: FP = 1 x {32, 64}ch, FP = 2 x {16, 32, 64}ch
+    assert len(das) == 198
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
