@@ -504,8 +504,9 @@ static bool tma_has128(const bm_das_geometry& g) {
 
 // channels per stage and stage count for the shared-memory share of one CTA
 // (fp frames per pass: every stage holds fp frames' windows)
-static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_t& smem) {
-  if (fp > 4) return false;
+static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_t& smem,
+                     int max_t = 128) {
+  if (fp > 8) return false;
   const int W = tma_window(g);
   const int per_sm = 512 / tma_cols(g);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
@@ -516,6 +517,7 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
     if (t > g.n_rx && t > 32) continue;
     if (t == 128 && (!tma_has128(g) || fp != 1)) continue;
     if (t == 16 && fp < 4) continue;  // 16-channel stages: four frames per pass only
+    if (t > max_t) continue;          // no kernel instantiated for this stage size
     if (only && t != only) continue;
     int n = kTmaMaxStages;
     while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw, fp).total > cap) --n;
@@ -569,17 +571,20 @@ static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
   // thread accumulates ft frames (FT)
   c.fp = c.ft = 1;
   if (g.rx_identity) {
-    const char* e = getenv("BM_DAS_FP");  // tuning override: 1 | 2
-    const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2
-    const int want_fp = e ? atoi(e) : 2, want_ft = e2 ? atoi(e2) : 2;
-    const bool ft2_ok = g.uniform && !g.t0_nonzero;
-    const int cand[3][2] = {{want_fp, want_ft}, {1, want_ft}, {want_fp, 1}};
+    const char* e = getenv("BM_DAS_FP");   // tuning override: 1 | 2
+    const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2 | 4 (the most tried)
+    const int want_fp = e && atoi(e) == 1 ? 1 : 2;
+    const int want_ft = e2 ? (atoi(e2) >= 4 ? 4 : atoi(e2) == 2 ? 2 : 1) : 4;
+    // several frames per thread: uniform apodisation, all-zero t0
+    const bool ftn_ok = g.uniform && !g.t0_nonzero;
+    // most frames per pass first; FP = 2 before FP = 1 at equal FT
+    const int cand[6][2] = {{want_fp, 4}, {1, 4}, {want_fp, 2}, {1, 2}, {want_fp, 1}, {1, 1}};
     for (const auto& cd : cand) {
-      const int f = cd[0] == 2 ? 2 : 1, t = cd[1] == 2 ? 2 : 1;
-      if (f * t == 1 || (t == 2 && !ft2_ok) || fpc < f * t) continue;
+      const int f = cd[0], t = cd[1];
+      if (t > want_ft || f * t == 1 || (t > 1 && !ftn_ok) || fpc < f * t) continue;
       int t2, n2;
       size_t s2;
-      if (tma_plan(g, f * t, t2, n2, s2)) {
+      if (tma_plan(g, f * t, t2, n2, s2, t == 4 ? 32 : 64)) {
         c.fp = f;
         c.ft = t;
         c.tjc = t2;
@@ -689,6 +694,19 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     k = table3[(fp == 2 ? 12 : 0) + (tjc == 64 ? 8 : tjc == 32 ? 4 : 0) + (lin ? 2 : 0) +
                (pw ? 1 : 0)];
     if (!k) return -1;
+  }
+  if (ft == 4) {
+    // four frames per thread, same apertures; rows: FP = 1 / 2 x 16 / 32-channel stages
+#define BM_TMA_FT4(J, F)                                                                   \
+  das_tma_kernel<false, false, false, true, J, false, F, 4>,                               \
+      das_tma_kernel<true, false, false, true, J, false, F, 4>,                            \
+      das_tma_kernel<false, true, false, true, J, false, F, 4>,                            \
+      das_tma_kernel<true, true, false, true, J, false, F, 4>
+    static const kfn table4[16] = {BM_TMA_FT4(16, 1), BM_TMA_FT4(32, 1), BM_TMA_FT4(16, 2),
+                                   BM_TMA_FT4(32, 2)};
+#undef BM_TMA_FT4
+    if (tjc > 32) return -1;
+    k = table4[(fp == 2 ? 8 : 0) + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
   }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
