@@ -69,6 +69,30 @@ def synth_frames(ctx, n_s, n_frames, seed0):
     return out
 
 
+def dropin_fps(ctx, grid, host, interp, n_frames=48, warmup=4):
+    """Frames/s a reference user sees calling the drop-in operator chain one
+    frame at a time: ``execute(build_graph(bmode_chain(...)), (RfFrame, ctx))``
+    with numpy RF in and the numpy display read back (pageable H2D/D2H and a
+    synchronisation per frame).  RfFrame construction (the reference's host
+    finiteness scan) happens before the clock, as in echopipe's own
+    benchmark()."""
+    import paper_1811_01566_b200 as bm
+
+    spec = bm.bmode_chain(interpolation=interp,
+                          grid={"x_positions": grid.x_positions.tolist(),
+                                "z_positions": grid.z_positions.tolist()})
+    graph = bm.build_graph(spec)
+    frames = [bm.RfFrame(host[i]) for i in range(min(len(host), 8))]
+    for i in range(warmup):
+        outs, _ = bm.execute(graph, (frames[i % len(frames)], ctx))
+        outs["dynamic_adjustment"].numpy()
+    t0 = time.perf_counter()
+    for i in range(n_frames):
+        outs, _ = bm.execute(graph, (frames[i % len(frames)], ctx))
+        outs["dynamic_adjustment"].numpy()
+    return n_frames / (time.perf_counter() - t0)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 100 ms by a
     background nvidia-smi loop (the recipe's clocks line) while running."""
@@ -229,7 +253,7 @@ def main():
             "config": {"workload": WORKLOAD, "frames_per_step": 1},
             "cpu_baseline": {"value": round(val, 4), "unit": "frames/s", "cores": cores,
                              "kind": "port",
-                             "sample": "1 cfg2 frame per step: oracle/ C DAS (pthreads, all "
+                             "sample": f"1 {args.config} frame per step: oracle/ C DAS (pthreads, all "
                                        "cores) + scipy.fft analytic + numpy dB"},
             "e2e": {"value": round(val, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}), flush=True)
@@ -319,6 +343,11 @@ def main():
         if world > 1:
             torch.distributed.destroy_process_group()
         return
+    if e2e is not None and world == 1:
+        e2e["dropin_per_frame_fps"] = round(dropin_fps(ctx, grid, host, args.interp), 1)
+        e2e["dropin_note"] = ("one frame per call through the reference-facing operator chain "
+                              "(numpy in, numpy display out, pageable copies); value above is "
+                              "the batched engine from pinned memory")
 
     # ---- roofline of the dominant kernel (DAS) ------------------------------
     peaks = {}

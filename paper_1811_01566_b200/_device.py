@@ -2,11 +2,50 @@
 
 from __future__ import annotations
 
+import threading
 import warnings
 
 import numpy as np
 
 from .types import _is_torch
+
+
+# numpy arrays at least this large go through a pinned staging buffer: a
+# host memcpy into page-locked memory plus a DMA at the link's full rate beats
+# the driver's pageable path (~19 vs ~55 GB/s H2D on the B200 box for an
+# 11.5 MB cfg2 frame)
+_STAGE_MIN_BYTES = 1 << 20
+_stage = threading.local()
+
+
+def _staged_h2d(src, device):
+    """Copy a contiguous CPU tensor to ``device`` through one of two per-thread
+    pinned buffers; the copy is enqueued on the current stream."""
+    import torch
+
+    pool = getattr(_stage, "pool", None)
+    if pool is None:
+        pool = _stage.pool = {"bufs": [None, None], "events": [None, None], "next": 0}
+    i = pool["next"]
+    pool["next"] ^= 1
+    nbytes = src.numel() * src.element_size()
+    buf = pool["bufs"][i]
+    if buf is None or buf.numel() < nbytes:
+        buf = pool["bufs"][i] = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),
+                                            dtype=torch.uint8, pin_memory=True)
+        pool["events"][i] = None
+    ev = pool["events"][i]
+    if ev is not None:
+        ev.synchronize()  # the DMA that last read this buffer has finished
+    stage = buf[:nbytes].view(src.dtype).view(src.shape)
+    stage.copy_(src)
+    out = torch.empty(src.shape, dtype=src.dtype, device=device)
+    with torch.cuda.device(device):
+        out.copy_(stage, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+    pool["events"][i] = ev
+    return out
 
 
 def to_device(a, device, dtype=None):
@@ -26,6 +65,8 @@ def to_device(a, device, dtype=None):
         src = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None and src.dtype != dtype:
         src = src.to(dtype)
+    if src.numel() * src.element_size() >= _STAGE_MIN_BYTES and torch.device(device).type == "cuda":
+        return _staged_h2d(src, torch.device(device))
     return src.to(device)
 
 

@@ -98,3 +98,24 @@ def test_seeded_benchmark_outputs_identical():
         assert (o1["dynamic_adjustment"].numpy().tobytes()
                 == o2["dynamic_adjustment"].numpy().tobytes())
     assert r1.timing.total_ms > 0
+
+
+def test_staged_host_to_device_copies_are_exact_and_do_not_alias():
+    """Large numpy inputs reach the device through two alternating pinned
+    staging buffers (_device._staged_h2d): every copy is exact, and a later
+    copy never overwrites the data of an earlier one still in flight."""
+    import torch
+
+    from paper_1811_01566_b200._device import to_device
+
+    rng = np.random.default_rng(3)
+    dev = torch.device("cuda", 0)
+    hosts = [rng.normal(size=(11, 128, 512)).astype(np.float32) for _ in range(5)]
+    outs = [to_device(h, dev) for h in hosts]          # 2.9 MB each: staged
+    small = to_device(hosts[0][:1, :1], dev)            # below the threshold: plain copy
+    torch.cuda.synchronize()
+    for h, o in zip(hosts, outs):
+        assert torch.equal(o.cpu(), torch.from_numpy(h))
+    assert torch.equal(small.cpu(), torch.from_numpy(hosts[0][:1, :1].copy()))
+    f64 = to_device(hosts[1].astype(np.float64), dev)
+    assert f64.dtype == torch.float64 and torch.equal(f64.cpu(), torch.from_numpy(hosts[1].astype(np.float64)))
