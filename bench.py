@@ -38,6 +38,10 @@ WORKLOADS = {
     "cfg1": "cfg1 STAI 64el x 64tx x 2048 samples -> 256x256, DAS+envelope+dB30, linear",
     "cfg2": "cfg2 PWI 128el x 11 angles x 2048 samples -> 512x512, DAS+envelope+dB30, linear",
     "cfg3": "cfg3 STAI 128el x 128tx x 4096 samples -> 1024x512, DAS+envelope+dB30, linear",
+    "sta-paper": "sta-paper STAI 128el x 128tx x 64 rx (centred map) x 2048 samples -> 2048x128, "
+                 "DAS+envelope+dB30, linear",
+    "pwi-paper": "pwi-paper PWI 192el x 11 angles x 2048 samples -> 512x128, DAS+envelope+dB30, "
+                 "linear",
 }
 WORKLOAD = WORKLOADS["cfg2"]
 
@@ -231,7 +235,8 @@ def main():
     ctx, grid, n_s = ME.config_geometry(args.config)
     global WORKLOAD
     WORKLOAD = WORKLOADS.get(args.config, WORKLOAD).replace("linear", args.interp)
-    frame_bytes = ctx.n_tx * ctx.n_elements * n_s * 4
+    n_rx = ctx.rx_channel_map.shape[1] if ctx.rx_channel_map is not None else ctx.n_elements
+    frame_bytes = ctx.n_tx * n_rx * n_s * 4
     img_bytes = grid.n_z * grid.n_x * 4
 
     if args.impl == "reference":
@@ -365,7 +370,7 @@ def main():
             traffic = prof["dram_bytes_per_frame"] * B
     except Exception:
         pass
-    contrib = B * ctx.n_tx * ctx.n_elements * grid.n_z * grid.n_x
+    contrib = B * ctx.n_tx * n_rx * grid.n_z * grid.n_x
     sm_mhz = clk["sm_mhz"] or 1965.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     # Rooflines of DAS, both measured on this B200

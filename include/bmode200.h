@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BMODE200_ABI_VERSION 1
+#define BMODE200_ABI_VERSION 2
 
 /* element type of every floating-point buffer of one call */
 enum { BM_F32 = 0, BM_F64 = 1 };
@@ -101,6 +101,10 @@ typedef struct bm_das_geometry {
   const int32_t* span;       /* [2 * n_z * n_x] inclusive active span (i0, i1)
                                 per pixel, from bm_das_aperture_span; NULL
                                 when f_number == 0 (all elements active)      */
+  int32_t rx_contig;         /* set by bm_das_prepare: 1 if every acquisition's
+                                channels are consecutive elements,
+                                rx_map[e][j] == rx_map[e][0] + j (identity maps
+                                and echopipe's centered_rx_map, types.py:319-333) */
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64

@@ -428,8 +428,11 @@ static int g4_window_bound(const bm_das_geometry* g, const double* elem_x, const
           if (m >= 0 && m < n_el) txr = std::max(txr, (double)rmax[m] - (double)rmin[m]);
         }
       }
+      // groups of 4 consecutive elements: aligned for identity maps, every
+      // start for the per-acquisition runs of a contiguous map
+      const int gstep = g->rx_identity ? 4 : 1;
       double grp = 0.0;
-      for (int m0 = 0; m0 < n_el; m0 += 4) {
+      for (int m0 = 0; m0 < n_el; m0 += gstep) {
         float lo = rmin[m0], hi = rmax[m0];
         for (int m = m0 + 1; m < std::min(m0 + 4, n_el); ++m) {
           lo = std::min(lo, rmin[m]);
@@ -452,6 +455,7 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->window_hint_g4 = 0;
   g->t0_nonzero = 1;
   g->rx_identity = 0;
+  g->rx_contig = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   // window bound of a tz x tx-pixel tile: tx delay range + rx delay range
   // (each <= k * tile diagonal) + margins
@@ -494,6 +498,14 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   for (int64_t i = 0; ident && i < (int64_t)g->n_tx * g->n_rx; ++i)
     if (rx_map[i] != (int)(i % g->n_rx)) ident = 0;
   g->rx_identity = ident;
+  int contig = g->n_rx <= g->n_elements;
+  for (int e = 0; contig && e < g->n_tx; ++e) {
+    const int32_t* r = rx_map + (int64_t)e * g->n_rx;
+    if (r[0] < 0 || r[0] + g->n_rx > g->n_elements) contig = 0;
+    for (int j = 1; contig && j < g->n_rx; ++j)
+      if (r[j] != r[0] + j) contig = 0;
+  }
+  g->rx_contig = contig;
   if (!(tabs < 4194304.0)) return BM_OK;  // outside the exact magic-number range
   if (W_wide > 4096) return BM_OK;
   g->window_hint = W;

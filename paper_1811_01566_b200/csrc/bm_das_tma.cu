@@ -47,7 +47,7 @@ struct TmaLayout {
   int tmin, rmin, metaK, metaM, txd, win, total;
   __host__ __device__ TmaLayout(int n_tx, int n_el, int tjc, int nst, int W, bool pw, int fp) {
     tmin = 256;  // [0,16) TMEM base, [64,128) full barriers, [128,192) empty barriers
-    rmin = (tmin + 16 * n_tx + 15) & ~15;
+    rmin = (tmin + 20 * n_tx + 15) & ~15;
     metaK = (rmin + 8 * n_el + 15) & ~15;
     metaM = metaK + 4 * tjc * nst * fp;
     txd = metaM + 4 * tjc * nst;
@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   float* tmax = tmin + n_tx;                                    // [n_tx]
   float* t0v = tmax + n_tx;                                     // [n_tx] fs*t0
   int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
+  int* rxb = txe + n_tx;  // [n_tx] first receive element of each transmit (IDMAP: run rxb + j)
   float* rmin = reinterpret_cast<float*>(smem_raw + lay.rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
   int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][FPP][TJC] gather base K
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   for (int e = tid; e < n_tx; e += NTH) {
     t0v[e] = reinterpret_cast<const float*>(g.t0_smp)[e];
     if (!PW) txe[e] = g.tx_elements[e];
+    rxb[e] = IDMAP ? g.rx_map[(int64_t)e * n_rx] : 0;
     if (PW) {
       const double ca = reinterpret_cast<const float*>(g.cos_a)[e];
       const double sa = reinterpret_cast<const float*>(g.sin_a)[e];
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         const int gi = lane + 32 * u;
         if (gi < ngr) {
           const int jj0 = gi * G;
-          int m = jb + jj0;
+          int m = (IDMAP ? rxb[e] : 0) + jb + jj0;
           float rlo = rmin[m];
           if (IDMAP) {  // G adjacent elements share the window
 #pragma unroll
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
 #undef BM_PAIR
           }
         };
-        const uint32_t tc = tlane + 2 * cur.cb * TJC;
+        const uint32_t tc = tlane + 2 * (rxb[cur.e] + cur.cb * TJC);
 #pragma unroll
         for (int h = 0; h < TJC; h += 16) {
           uint32_t r[32], w[32];
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         }
       } else {
         for (int jj = 0; jj < jn; ++jj) {
-          const int m = IDMAP ? cur.cb * TJC + jj : MMc[jj];
+          const int m = IDMAP ? rxb[cur.e] + cur.cb * TJC + jj : MMc[jj];
           channel((VT)tm_ld2(tlane + 2 * m), WT ? (VT)tm_ld2(tlane + 2 * n_el + 2 * m) : 0ull,
                   (uint32_t)MKc[jj]);
         }
@@ -486,7 +488,7 @@ static EncodeTiledFn encode_tiled() {
 // row stride of the staged windows: one channel per box (128-B aligned rows)
 // or 4 adjacent channels per box sharing one window start
 static int tma_window(const bm_das_geometry& g) {
-  return g.rx_identity && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
+  return g.rx_contig && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
 }
 
 // TMEM columns of one CTA: delay pairs (2 per element) plus, with
@@ -499,7 +501,7 @@ static int tma_cols(const bm_das_geometry& g) {
 // 128-channel stages exist for the uniform linear identity-map no-t0 kernels
 // (the BASELINE configurations): one stage boundary per 128 channels
 static bool tma_has128(const bm_das_geometry& g) {
-  return g.uniform && g.interp == BM_LINEAR && !g.t0_nonzero && g.rx_identity;
+  return g.uniform && g.interp == BM_LINEAR && !g.t0_nonzero && g.rx_contig;
 }
 
 // channels per stage and stage count for the shared-memory share of one CTA
@@ -534,7 +536,7 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || g.window_hint <= 0 || tma_window(g) > 256) return 0;
   if (!g.uniform && (4 * g.n_elements > 512 || (g.window == BM_HANN && !g.hann))) return 0;
-  if (g.rx_identity && g.window_hint_g4 <= 0) return 0;  // 4-channel boxes need the bound
+  if (g.rx_contig && g.window_hint_g4 <= 0) return 0;  // 4-channel boxes need the bound
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;  // 16-B TMA strides
   if (2 * g.n_elements > 512) return 0;                       // pair layout in TMEM
   if ((int64_t)g.n_tx * g.n_rx > 0x7fffffffLL) return 0;
@@ -570,7 +572,7 @@ static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
   // enough frames: fp consumer warp groups share one delay table (FP), each
   // thread accumulates ft frames (FT)
   c.fp = c.ft = 1;
-  if (g.rx_identity) {
+  if (g.rx_contig) {
     const char* e = getenv("BM_DAS_FP");   // tuning override: 1 | 2
     const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2 | 4 (the most tried)
     const int want_fp = e && atoi(e) == 1 ? 1 : 2;
@@ -624,7 +626,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   cuuint64_t dims[3] = {(cuuint64_t)g.n_samples, (cuuint64_t)g.n_tx * g.n_rx,
                         (cuuint64_t)n_frames};
   cuuint64_t strides[2] = {(cuuint64_t)g.n_samples * 4, (cuuint64_t)fstride * 4};
-  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_identity ? 4u : 1u, (cuuint32_t)(fp * ft)};
+  cuuint32_t box[3] = {(cuuint32_t)W, g.rx_contig ? 4u : 1u, (cuuint32_t)(fp * ft)};
   cuuint32_t estr[3] = {1, 1, 1};
   if (encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(rf), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -655,7 +657,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                                 BM_TMA_ROW(32, true), BM_TMA_ROW(64, true)};
 #undef BM_TMA_ROW
   kfn k = table[(g.uniform ? 0 : 32) + (tjc >= 64 ? 16 : 0) +
-                ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) | (g.rx_identity ? 1 : 0))];
+                ((pw ? 8 : 0) | (lin ? 4 : 0) | (g.t0_nonzero ? 2 : 0) | (g.rx_contig ? 1 : 0))];
   if (tjc == 128) {
     if (!tma_has128(g)) return -1;
     k = pw ? das_tma_kernel<true, true, false, true, 128> : das_tma_kernel<false, true, false, true, 128>;

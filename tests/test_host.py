@@ -33,7 +33,7 @@ def test_library_built_for_sm100a_and_exports_header_symbols():
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES), "ctypes signatures out of sync with the header"
     lib.bm_abi_version.restype = ctypes.c_int
-    assert lib.bm_abi_version() == 1
+    assert lib.bm_abi_version() == 2
     lib.bm_error_string.restype = ctypes.c_char_p
     assert lib.bm_error_string(4) == b"analytic signal needs axis length >= 2"
 
@@ -46,8 +46,10 @@ def test_library_contains_sm100a_code():
 
 
 def test_geometry_struct_layout():
-    # 16 int32 + 2 double + 10 pointers, no padding surprises
-    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8
+    # 16 int32 + 2 double + 10 pointers + rx_contig (int32, then tail padding
+    # to the 8-B struct alignment), as a C compiler lays out bm_das_geometry
+    assert N.DasGeometry.rx_contig.offset == 16 * 4 + 2 * 8 + 10 * 8
+    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 8
 
 
 def test_invalid_arguments_rejected_without_gpu():
