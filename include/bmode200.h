@@ -105,6 +105,10 @@ typedef struct bm_das_geometry {
                                 channels are consecutive elements,
                                 rx_map[e][j] == rx_map[e][0] + j (identity maps
                                 and echopipe's centered_rx_map, types.py:319-333) */
+  int32_t tile_ls;           /* set by bm_das_prepare: TMA-kernel tile shape for
+                                contiguous maps, log2 of the lane-block width:
+                                3 = 16 x 16 pixels (lane blocks 4 x 8), 2 = 32 x 8,
+                                1 = 64 x 4, 4 = 8 x 32; window_hint_g4 is for it */
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64

@@ -37,7 +37,7 @@ class DasGeometry(ctypes.Structure):
         ("elem_x", ctypes.c_void_p), ("x_pos", ctypes.c_void_p), ("z_pos", ctypes.c_void_p),
         ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),
         ("rx_map", ctypes.c_void_p), ("t0_smp", ctypes.c_void_p), ("hann", ctypes.c_void_p),
-        ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32),
+        ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32), ("tile_ls", ctypes.c_int32),
     ]
 
 

@@ -370,7 +370,7 @@ int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride,
 // rounding of the device's sums and floors.  Returns 0 if the transmit
 // geometry cannot be read back.
 static int g4_window_bound(const bm_das_geometry* g, const double* elem_x, const double* x,
-                           const double* z) {
+                           const double* z, int TZ = 16, int TX = 16) {
   const int n_el = g->n_elements, n_tx = g->n_tx;
   std::vector<float> ca(n_tx), sa(n_tx);
   std::vector<int> te(n_tx);
@@ -402,10 +402,10 @@ static int g4_window_bound(const bm_das_geometry* g, const double* elem_x, const
   const float kf = (float)k;
   std::vector<float> rmin(n_el), rmax(n_el);
   double need = 0.0;
-  for (int tz0 = 0; tz0 < g->n_z; tz0 += 16)
-    for (int tx0 = 0; tx0 < g->n_x; tx0 += 16) {
-      const double x0 = x[tx0], x1 = x[std::min(tx0 + 16, g->n_x) - 1];
-      const double z0 = z[tz0], z1 = z[std::min(tz0 + 16, g->n_z) - 1];
+  for (int tz0 = 0; tz0 < g->n_z; tz0 += TZ)
+    for (int tx0 = 0; tx0 < g->n_x; tx0 += TX) {
+      const double x0 = x[tx0], x1 = x[std::min(tx0 + TX, g->n_x) - 1];
+      const double z0 = z[tz0], z1 = z[std::min(tz0 + TZ, g->n_z) - 1];
       const float x0f = (float)x0, x1f = (float)x1, z0f = (float)z0, z1f = (float)z1;
       for (int m = 0; m < n_el; ++m) {
         const float xm = (float)elem_x[m];
@@ -456,6 +456,7 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->t0_nonzero = 1;
   g->rx_identity = 0;
   g->rx_contig = 0;
+  g->tile_ls = 3;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   // window bound of a tz x tx-pixel tile: tx delay range + rx delay range
   // (each <= k * tile diagonal) + margins
@@ -506,20 +507,46 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
       if (r[j] != r[0] + j) contig = 0;
   }
   g->rx_contig = contig;
-  if (!(tabs < 4194304.0)) return BM_OK;  // outside the exact magic-number range
+  // 4 adjacent elements share one window (a 4-row TMA box): rx delays are
+  // k-Lipschitz in the element position, so the union spans at most
+  // W + k * (x[m+3] - x[m]); rounded to 8 samples (128-B aligned box rows)
+  // and tightened by the per-tile evaluation where the geometry can be read.
+  // Per TMA tile shape ls: lane blocks of (32 >> ls) x (1 << ls) pixels,
+  // tiles of 4 (32 >> ls) x 2 (1 << ls).
+  double ext = 0.0;
+  for (int m = 0; m + 3 < g->n_elements; ++m) ext = fmax(ext, fabs(elem_x[m + 3] - elem_x[m]));
+  auto g4_for = [&](int ls) {
+    const int TZ = 4 * (32 >> ls), TX = 2 << ls;
+    const int wg = ((int)ceil(bound(TZ, TX) + k * ext + 4.0) + 7) & ~7;
+    const int exact = g4_window_bound(g, elem_x, x, z, TZ, TX);
+    return exact > 0 && exact < wg ? exact : wg;
+  };
+  // contiguous maps pick the tile whose staged window is smallest; another
+  // shape than 16 x 16 only for a >= 20 % smaller window (measured: sta-paper
+  // 64 x 4 tiles W 96 vs 192, 0.77 -> 0.53 ms/frame; cfg1 8 x 32 W 128 vs 152
+  // is 2 % slower)
+  int ls = 3, wbest = g->n_elements >= 4 ? g4_for(3) : 0;
+  if (contig && g->n_elements >= 4) {
+    const char* e = getenv("BM_DAS_TILE");  // override: 1 (64 x 4) .. 4 (8 x 32)
+    const int force = e ? atoi(e) : 0;
+    if (force >= 1 && force <= 4) {
+      ls = force;
+      wbest = g4_for(ls);
+    } else {
+      for (int c : {1, 2, 4}) {
+        const int w = g4_for(c);
+        if (w * 5 <= wbest * 4 && w < wbest) {
+          ls = c;
+          wbest = w;
+        }
+      }
+    }
+  }
+  g->tile_ls = ls;
+  if (!(tabs - W + (wbest > W ? wbest : W) < 4194304.0)) return BM_OK;  // outside the exact magic-number range
   if (W_wide > 4096) return BM_OK;
   g->window_hint = W;
   g->window_hint_wide = W_wide;
-  // 4 adjacent elements share one window: rx delays are k-Lipschitz in the
-  // element position, so the union spans at most W + k * (x[m+3] - x[m]);
-  // rounded to 8 samples (128-B aligned 4-row TMA boxes)
-  if (g->n_elements >= 4) {
-    double ext = 0.0;
-    for (int m = 0; m + 3 < g->n_elements; ++m) ext = fmax(ext, fabs(elem_x[m + 3] - elem_x[m]));
-    const int wg = (int)ceil(W + k * ext + 4.0);
-    g->window_hint_g4 = (wg + 7) & ~7;
-    const int exact = g4_window_bound(g, elem_x, x, z);  // tighter where it can be read
-    if (exact > 0 && exact < g->window_hint_g4) g->window_hint_g4 = exact;
-  }
+  if (g->n_elements >= 4) g->window_hint_g4 = wbest;
   return BM_OK;
 }

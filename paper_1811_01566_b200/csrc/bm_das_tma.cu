@@ -40,6 +40,7 @@ struct TmaArgs {
   int W;          // samples per channel window (multiple of 32: 128-B aligned rows)
   int nst;        // pipeline stages (2 .. kTmaMaxStages)
   int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
+  int ls;         // tile shape: lane blocks of (32 >> ls) x (1 << ls) pixels
 };
 
 // shared-memory carve (bytes), identical on host and device
@@ -125,7 +126,10 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   constexpr int NTH = 32 * (4 * FP + 1), NC = 128;  // threads, pixel-pair threads
   constexpr int NCW = 4 * FP;                        // consumer warps
   constexpr int FPP = FP * FT;                       // frames per pass
-  constexpr int TZk = 16, TXk = 16;
+  // tile = 2 x 2 warp blocks; a warp block = pixel rows A (lane / CA) and B
+  // (A + RA) of a RA x CA lane block (ls = 3: 16 x 16 tiles of 8 x 8 blocks)
+  const int CA = 1 << a.ls, RA = 32 >> a.ls;
+  const int TZk = 4 * RA, TXk = 2 * CA;
   constexpr int G = IDMAP ? 4 : 1;  // receive channels per TMA box (rows of W samples)
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx;
@@ -155,8 +159,8 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   const int ctid = tid & (NC - 1);          // consumer: pixel-pair thread index
   const int tiles_x = (g.n_x + TXk - 1) / TXk;
   const int tz0 = (blockIdx.x / tiles_x) * TZk, tx0 = (blockIdx.x % tiles_x) * TXk;
-  const int col = tx0 + (warp & 1) * 8 + (lane & 7);
-  const int rowA = tz0 + ((warp >> 1) & 1) * 8 + (lane >> 3), rowB = rowA + 4;
+  const int col = tx0 + (warp & 1) * CA + (lane & (CA - 1));
+  const int rowA = tz0 + ((warp >> 1) & 1) * 2 * RA + (lane >> a.ls), rowB = rowA + RA;
   const int colc = min(col, g.n_x - 1);
   const int rAc = min(rowA, g.n_z - 1), rBc = min(rowB, g.n_z - 1);
 
@@ -491,6 +495,16 @@ static int tma_window(const bm_das_geometry& g) {
   return g.rx_contig && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
 }
 
+// tile shape of a launch: contiguous maps use the prepared shape, other maps
+// the 16 x 16 tiles window_hint bounds
+static int tma_ls(const bm_das_geometry& g) {
+  return g.rx_contig && g.tile_ls >= 1 && g.tile_ls <= 4 ? g.tile_ls : 3;
+}
+static int tma_tiles(const bm_das_geometry& g) {
+  const int ls = tma_ls(g), TZ = 4 * (32 >> ls), TX = 2 << ls;
+  return ((g.n_z + TZ - 1) / TZ) * ((g.n_x + TX - 1) / TX);
+}
+
 // TMEM columns of one CTA: delay pairs (2 per element) plus, with
 // non-uniform apodisation, weight pairs (2 more per element)
 static int tma_cols(const bm_das_geometry& g) {
@@ -555,7 +569,7 @@ struct TmaChoice {
 };
 static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
   if (!tma_plan(g, 1, c.tjc, c.nst, c.smem)) return false;
-  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
+  const int tiles = tma_tiles(g);
   const int per_sm = 512 / tma_cols(g);
   // frames per CTA: amortise the per-CTA delay-table build over a frame
   // group while keeping >= 4 waves of CTAs for load balance
@@ -617,7 +631,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   TmaChoice c;
   if (!tma_choose(g, n_frames, c)) return -1;
   const int W = tma_window(g);
-  const int tiles = ((g.n_z + 15) / 16) * ((g.n_x + 15) / 16);
+  const int tiles = tma_tiles(g);
   const int fpc = c.fpc, fp = c.fp, ft = c.ft, tjc = c.tjc, nst = c.nst;
   const size_t smem = c.smem;
   // RF as a 3-D tensor: samples x (transmit, channel) rows x frames
@@ -633,7 +647,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  TmaArgs a{g, (float*)out, out_stride, n_frames, fpc, W, nst, tma_cols(g)};
+  TmaArgs a{g, (float*)out, out_stride, n_frames, fpc, W, nst, tma_cols(g), tma_ls(g)};
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
 #define BM_TMA_ROW(J, WT)                                                                  \

@@ -46,9 +46,10 @@ def test_library_contains_sm100a_code():
 
 
 def test_geometry_struct_layout():
-    # 16 int32 + 2 double + 10 pointers + rx_contig (int32, then tail padding
-    # to the 8-B struct alignment), as a C compiler lays out bm_das_geometry
+    # 16 int32 + 2 double + 10 pointers + rx_contig + tile_ls (int32), as a C
+    # compiler lays out bm_das_geometry
     assert N.DasGeometry.rx_contig.offset == 16 * 4 + 2 * 8 + 10 * 8
+    assert N.DasGeometry.tile_ls.offset == 16 * 4 + 2 * 8 + 10 * 8 + 4
     assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 8
 
 
