@@ -415,7 +415,7 @@ def main():
     }
 
     cpu = None
-    if not args.no_cpu and args.cpu_seconds > 0:
+    if not args.no_cpu and args.cpu_seconds > 0 and world == 1:  # rank 0 at N=1 only
         fps, cores, n, el = cpu_reference(ctx, grid, host[:4], args.cpu_seconds, args.interp)
         cpu = {"value": round(fps, 4), "unit": "frames/s", "cores": cores, "kind": "port",
                "sample": f"{n} {args.config} frames in {el:.1f}s: oracle/ C DAS (pthreads) + scipy.fft "
