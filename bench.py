@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--frames", type=int, default=32, help="frames per GPU per step")
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--interp", default="linear")
+    ap.add_argument("--window", default="rectangular", choices=["rectangular", "hann"],
+                    help="receive apodisation window (ApodizationSpec)")
+    ap.add_argument("--f-number", type=float, default=0.0,
+                    help="dynamic-aperture f-number (0: all elements)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -280,7 +284,10 @@ def main():
 
     B = args.frames
     host = synth_frames(ctx, n_s, B, seed0=rank * B)
-    eng = bm.engine.BmodeEngine(ctx, grid, interp=args.interp, dtype=np.float32)
+    apod = bm.ApodizationSpec(args.window, args.f_number)
+    eng = bm.engine.BmodeEngine(ctx, grid, apod=apod, interp=args.interp, dtype=np.float32)
+    if not eng.plan.uniform:
+        WORKLOAD = WORKLOAD + f", {args.window} F={args.f_number:g}"
     rf = torch.from_numpy(host).to(dev)
     out = torch.empty((B, grid.n_z, grid.n_x), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -386,7 +393,12 @@ def main():
     #    (t, floor, k0, a, 1-a) + 4 per frame, nearest 3 (t, +0.5, floor) + 1.
     shape = eng.plan.launch_shape(n_s, B, args.interp) or {"ft": 1}
     ft = shape["ft"]
-    ops = (5.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 1.0)
+    #    Non-uniform apodisation adds w*(1-a), w*a per (pixel, channel)
+    #    (linear) or one w*x per frame (nearest).
+    if eng.plan.uniform:
+        ops = (5.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 1.0)
+    else:
+        ops = (7.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 2.0)
     gb = 8 if args.interp == "linear" else 4
     t_fp32 = contrib * ops / (n_sm * 128 * sm_mhz * 1e6)
     t_lds = contrib * gb / (n_sm * 128 * sm_mhz * 1e6)

@@ -591,13 +591,15 @@ static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
     const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2 | 4 (the most tried)
     const int want_fp = e && atoi(e) == 1 ? 1 : 2;
     const int want_ft = e2 ? (atoi(e2) >= 4 ? 4 : atoi(e2) == 2 ? 2 : 1) : 4;
-    // several frames per thread: uniform apodisation, all-zero t0
-    const bool ftn_ok = g.uniform && !g.t0_nonzero;
+    // several frames per thread: all-zero t0; non-uniform apodisation (its
+    // w*(1-a), w*a shared by the frames too) with four frames per thread
+    const bool ftn_ok = !g.t0_nonzero;
     // most frames per pass first; FP = 2 before FP = 1 at equal FT
     const int cand[6][2] = {{want_fp, 4}, {1, 4}, {want_fp, 2}, {1, 2}, {want_fp, 1}, {1, 1}};
     for (const auto& cd : cand) {
       const int f = cd[0], t = cd[1];
       if (t > want_ft || f * t == 1 || (t > 1 && !ftn_ok) || fpc < f * t) continue;
+      if (t == 2 && !g.uniform) continue;  // not instantiated
       int t2, n2;
       size_t s2;
       if (tma_plan(g, f * t, t2, n2, s2, t == 4 ? 32 : 64)) {
@@ -712,17 +714,21 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     if (!k) return -1;
   }
   if (ft == 4) {
-    // four frames per thread, same apertures; rows: FP = 1 / 2 x 16 / 32-channel stages
-#define BM_TMA_FT4(J, F)                                                                   \
-  das_tma_kernel<false, false, false, true, J, false, F, 4>,                               \
-      das_tma_kernel<true, false, false, true, J, false, F, 4>,                            \
-      das_tma_kernel<false, true, false, true, J, false, F, 4>,                            \
-      das_tma_kernel<true, true, false, true, J, false, F, 4>
-    static const kfn table4[16] = {BM_TMA_FT4(16, 1), BM_TMA_FT4(32, 1), BM_TMA_FT4(16, 2),
-                                   BM_TMA_FT4(32, 2)};
+    // four frames per thread, contiguous maps, no t0, uniform and weighted;
+    // rows: uniform / weighted x FP = 1 / 2 x 16 / 32-channel stages
+#define BM_TMA_FT4(J, F, WT)                                                               \
+  das_tma_kernel<false, false, false, true, J, WT, F, 4>,                                  \
+      das_tma_kernel<true, false, false, true, J, WT, F, 4>,                               \
+      das_tma_kernel<false, true, false, true, J, WT, F, 4>,                               \
+      das_tma_kernel<true, true, false, true, J, WT, F, 4>
+    static const kfn table4[32] = {
+        BM_TMA_FT4(16, 1, false), BM_TMA_FT4(32, 1, false), BM_TMA_FT4(16, 2, false),
+        BM_TMA_FT4(32, 2, false), BM_TMA_FT4(16, 1, true),  BM_TMA_FT4(32, 1, true),
+        BM_TMA_FT4(16, 2, true),  BM_TMA_FT4(32, 2, true)};
 #undef BM_TMA_FT4
     if (tjc > 32) return -1;
-    k = table4[(fp == 2 ? 8 : 0) + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
+    k = table4[(g.uniform ? 0 : 16) + (fp == 2 ? 8 : 0) + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) +
+               (pw ? 1 : 0)];
   }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)

@@ -165,7 +165,8 @@ def test_no_contracted_fma_in_das_kernels():
     # + 20 two-frames-per-thread tma (uniform identity map, no t0) x {STA, PW} x
     # {nearest, linear}: FP = 1 x {32, 64}ch, FP = 2 x {16, 32, 64}ch
     # + 16 four-frames-per-thread tma, same apertures, FP = 1 / 2 x {16, 32}ch
-    assert len(das) == 214
+    # + 16 of them weighted (Hann / F-number)
+    assert len(das) == 230
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
