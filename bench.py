@@ -378,6 +378,15 @@ def main():
     except Exception:
         pass
     contrib = B * ctx.n_tx * n_rx * grid.n_z * grid.n_x
+    span = eng.plan._bufs.get("span")
+    if span is not None and eng.plan._geom.rx_identity:
+        # F-number gate: terms outside a pixel's active span have weight 0 and
+        # are exact zeros the kernel may skip, so the algorithmic work is the
+        # active contributions (identity / contiguous maps: the span clipped
+        # to the elements each transmit records)
+        sp = span.view(-1, 2).to(torch.int64)
+        lo, hi = sp[:, 0].clamp(min=0), sp[:, 1].clamp(max=ctx.n_elements - 1)
+        contrib = int(B * ctx.n_tx * (hi - lo + 1).clamp(min=0).sum().item())
     sm_mhz = clk["sm_mhz"] or 1965.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     # Rooflines of DAS, both measured on this B200

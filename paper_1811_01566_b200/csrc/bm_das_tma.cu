@@ -47,8 +47,9 @@ struct TmaArgs {
 struct TmaLayout {
   int tmin, rmin, metaK, metaM, txd, win, total;
   __host__ __device__ TmaLayout(int n_tx, int n_el, int tjc, int nst, int W, bool pw, int fp) {
-    tmin = 256;  // [0,16) TMEM base, [64,128) full barriers, [128,192) empty barriers
-    rmin = (tmin + 20 * n_tx + 15) & ~15;
+    tmin = 256;  // [0,16) TMEM base, [16,24) active element span, [64,128) full
+                 // barriers, [128,192) empty barriers
+    rmin = (tmin + 28 * n_tx + 15) & ~15;
     metaK = (rmin + 8 * n_el + 15) & ~15;
     metaM = metaK + 4 * tjc * nst * fp;
     txd = metaM + 4 * tjc * nst;
@@ -145,6 +146,9 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   float* t0v = tmax + n_tx;                                     // [n_tx] fs*t0
   int* txe = reinterpret_cast<int*>(t0v + n_tx);                // [n_tx] STA tx element
   int* rxb = txe + n_tx;  // [n_tx] first receive element of each transmit (IDMAP: run rxb + j)
+  int* cblo = rxb + n_tx;  // [n_tx] SKIP: first / last stage chunk of each transmit
+  int* cbhi = cblo + n_tx;
+  int* espan = reinterpret_cast<int*>(smem_raw + 16);  // SKIP: union of the tile's active spans
   float* rmin = reinterpret_cast<float*>(smem_raw + lay.rmin);  // [n_el]
   float* rmax = rmin + n_el;                                    // [n_el]
   int* metaK = reinterpret_cast<int*>(smem_raw + lay.metaK);    // [nst][FPP][TJC] gather base K
@@ -152,6 +156,11 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   u64* txd_s = reinterpret_cast<u64*>(smem_raw + lay.txd);      // PW: [n_tx][128]
   const uint32_t win_s = smem_s + (uint32_t)lay.win;            // [nst][TJC/G][FPP][G][W] f32
 
+  // SKIP: with an F-number gate (g.span) every element outside the union of
+  // the tile's active spans has weight 0 for all its pixels, so its terms
+  // are exact zeros (x is finite, acc never -0: acc + (+-0) == acc) and the
+  // stages of channels outside it are neither loaded nor computed
+  constexpr bool SKIP = WT && IDMAP;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == NCW;
@@ -174,6 +183,10 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   if (warp == 0) {
     tm_alloc(smem_s, (uint32_t)a.tmem_cols);
     tm_relinquish();
+  }
+  if (SKIP && tid == 0) {
+    espan[0] = n_el;
+    espan[1] = -1;
   }
   if (producer && lane == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -216,6 +229,15 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       };
       const float* hA = row(i0A, i1A);
       const float* hB = row(i0B, i1B);
+      if (SKIP && slot == 0) {
+        int lo = n_el, hi = -1;
+        if (i0A <= i1A) lo = min(lo, i0A), hi = max(hi, i1A);
+        if (i0B <= i1B) lo = min(lo, i0B), hi = max(hi, i1B);
+        if (hi >= 0) {
+          atomicMin(&espan[0], max(lo, 0));
+          atomicMax(&espan[1], min(hi, n_el - 1));
+        }
+      }
       for (int m = slot; m < n_el; m += FP) {
         const float wA = (m >= i0A && m <= i1A) ? (hA ? hA[m - i0A] : 1.0f) : 0.0f;
         const float wB = (m >= i0B && m <= i1B) ? (hB ? hB[m - i0B] : 1.0f) : 0.0f;
@@ -272,11 +294,57 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   const int n_chunks = (n_rx + TJC - 1) / TJC;
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
-  const int Q = ((f_count + FPP - 1) / FPP) * n_tx * n_chunks;  // passes x transmits x stages
+  const int n_pass = (f_count + FPP - 1) / FPP;
+  int Q = n_pass * n_tx * n_chunks;  // passes x transmits x stages
+  int e_first = 0, e_last = n_tx - 1;
+  if (SKIP) {
+    // per-transmit stage range over the active channels; an all-zero tile
+    // still runs transmit 0's first stage (its terms are zeros)
+    const int elo = espan[0], ehi = espan[1];
+    for (int e = tid; e < n_tx; e += NTH) {
+      const int jlo = max(0, elo - rxb[e]), jhi = min(n_rx - 1, ehi - rxb[e]);
+      cblo[e] = jlo <= jhi ? jlo / TJC : 1;
+      cbhi[e] = jlo <= jhi ? jhi / TJC : 0;
+    }
+    __syncthreads();
+    int tot = 0;
+    e_first = -1;
+    for (int e = 0; e < n_tx; ++e)
+      if (cblo[e] <= cbhi[e]) {
+        tot += cbhi[e] - cblo[e] + 1;
+        if (e_first < 0) e_first = e;
+        e_last = e;
+      }
+    if (e_first < 0) {
+      __syncthreads();
+      if (tid == 0) cblo[0] = cbhi[0] = 0;
+      __syncthreads();
+      e_first = e_last = 0;
+      tot = 1;
+    }
+    Q = n_pass * tot;
+  }
+  // stage cursor: (pass, transmit, chunk); SKIP walks each transmit's range
+  auto advance = [&](Cursor& c) {
+    if (!SKIP) {
+      c.next(n_chunks, n_tx);
+      return;
+    }
+    if (++c.cb > cbhi[c.e]) {
+      do {
+        if (++c.e == n_tx) {
+          c.e = 0;
+          ++c.fl;
+        }
+      } while (cblo[c.e] > cbhi[c.e]);
+      c.cb = cblo[c.e];
+    }
+  };
+  const Cursor c0{0, e_first, SKIP ? cblo[e_first] : 0, 0};
 
   if (producer) {
     // ================= producer warp: window starts + TMA issue
-    Cursor cu{0, 0, 0, 0};
+    Cursor cu = c0;
     int s = 0, r = 0;  // stage, round (q = r * nst + s)
     for (int q = 0; q < Q; ++q) {
       // round r >= 1 reuses stage s: wait for the consumers' release of round r-1
@@ -328,7 +396,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         mbar_arrive_tx(bar, (uint32_t)(ngr * G * FPP * W * 4));
       else
         mbar_arrive(bar);
-      cu.next(n_chunks, n_tx);
+      advance(cu);
       if (++s == nst) {
         s = 0;
         ++r;
@@ -344,12 +412,12 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     VT txd = acc[0], t0e2 = acc[0];
     // the thread's frame i > 0 sits i frame planes ({G, W} floats) after frame 0
     const uint32_t FOFF = (uint32_t)(G * W) * 4u;
-    Cursor cur{0, 0, 0, 0};
+    Cursor cur = c0;
     int s = 0;
     uint32_t ph = 0;
     for (int q = 0; q < Q; ++q) {
       mbar_wait(full_s + 8 * s, ph);
-      if (cur.cb == 0) {
+      if (cur.cb == (SKIP ? cblo[cur.e] : 0)) {  // first stage of a transmit
         if (PW)
           txd = (VT)txd_s[cur.e * NC + ctid];
         else
@@ -436,7 +504,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_s + 8 * s);  // stage s may be refilled
 
-      if (cur.e == n_tx - 1 && cur.cb == n_chunks - 1) {  // frame complete
+      if (cur.e == e_last && cur.cb == (SKIP ? cbhi[e_last] : n_chunks - 1)) {  // pass complete
 #pragma unroll
         for (int i = 0; i < FT; ++i) {
           const int fl = cur.fl * FPP + slot * FT + i;  // this thread's frame in the CTA's group
@@ -450,7 +518,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
           acc[i] = L::splat(0.0f);
         }
       }
-      cur.next(n_chunks, n_tx);
+      advance(cur);
       if (++s == nst) {
         s = 0;
         ph ^= 1;
