@@ -202,6 +202,8 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   const uint32_t tbase = *tmem_slot;
   const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
 
+  // SKIP: union of the active spans of this warp's 64 pixels (warp-uniform)
+  int wlo = 0, whi = n_el - 1;
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
   if (!producer) {
     // the FP warps sharing a lane quarter split the elements
@@ -229,14 +231,18 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       };
       const float* hA = row(i0A, i1A);
       const float* hB = row(i0B, i1B);
-      if (SKIP && slot == 0) {
+      if (SKIP) {
         int lo = n_el, hi = -1;
         if (i0A <= i1A) lo = min(lo, i0A), hi = max(hi, i1A);
         if (i0B <= i1B) lo = min(lo, i0B), hi = max(hi, i1B);
-        if (hi >= 0) {
-          atomicMin(&espan[0], max(lo, 0));
-          atomicMax(&espan[1], min(hi, n_el - 1));
+        lo = max(lo, 0);
+        hi = min(hi, n_el - 1);
+        if (slot == 0 && hi >= 0) {
+          atomicMin(&espan[0], lo);
+          atomicMax(&espan[1], hi);
         }
+        wlo = __reduce_min_sync(0xffffffffu, lo);
+        whi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi + 1)) - 1;
       }
       for (int m = slot; m < n_el; m += FP) {
         const float wA = (m >= i0A && m <= i1A) ? (hA ? hA[m - i0A] : 1.0f) : 0.0f;
@@ -480,6 +486,10 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         const uint32_t tc = tlane + 2 * (rxb[cur.e] + cur.cb * TJC);
 #pragma unroll
         for (int h = 0; h < TJC; h += 16) {
+          if (SKIP) {  // 16 channels outside every pixel's aperture of this warp: zeros
+            const int m0 = rxb[cur.e] + cur.cb * TJC + h;
+            if (m0 > whi || m0 + 15 < wlo) continue;
+          }
           uint32_t r[32], w[32];
           tm_ld32_issue(tc + 2 * h, r);
           if (WT) {
