@@ -8,20 +8,24 @@
 //    of the cp.async window copies and meets the others at one __syncthreads
 //    per chunk.  ncu (profiles/r01_das_tmem_ncu.txt) puts ~35 % of the warp
 //    samples of that kernel outside the gather/interpolate loop.
-//  * here a fifth PRODUCER warp owns all of it: per chunk of TJC receive
-//    channels it computes each channel's window start, publishes the gather
-//    base K, and issues one cp.async.bulk.tensor (TMA) per channel window
-//    [ws, ws + W) of trace (frame, e, j).  TMA's out-of-bounds fill writes
-//    exact zeros for samples outside [0, n_s) -- the reference's sentinel
-//    semantics (beamform.py:127-137) without a slow path.  The four CONSUMER
-//    warps only wait on the stage's full barrier, gather and interpolate, and
+//  * here a PRODUCER warp owns all of it: per stage of TJC receive channels
+//    it computes each 4-channel group's window start, publishes the gather
+//    bases K, and issues one cp.async.bulk.tensor (TMA) box {W samples, 4
+//    traces, frames of the pass} per group (one trace per box for general
+//    receive maps).  TMA's out-of-bounds fill writes exact zeros for samples
+//    outside [0, n_s) -- the reference's sentinel semantics
+//    (beamform.py:127-137) without a slow path.  The CONSUMER warps (4 x FP)
+//    only wait on the stage's full barrier, gather and interpolate, and
 //    release the stage through its empty barrier: no CTA-wide barrier in the
 //    loop.
 //
-// Tile and lane layout are das_tmem_kernel's PAIR layout: 16 x 16 pixels per
-// CTA, thread (warp w < 4, lane l) owns pixels (row l/8, col l%8) and
-// (row l/8 + 4, col l%8) of its warp's 8 x 8 block, TMEM lane 32w + l holds
-// the pair's delays to element m in columns 2m, 2m+1.
+// Tile and lane layout: 2 x 2 warp blocks per CTA; thread (warp w, lane l)
+// owns pixels A (row l >> ls, col l & (2^ls - 1) of its block) and B (A +
+// 32 >> ls rows), ls = 3 giving 16 x 16 tiles of 8 x 8 blocks (tile_ls picks
+// 32 x 8, 64 x 4 or 8 x 32 for other grids).  TMEM lane 32 (w & 3) + l holds
+// the pair's delays to element m in columns 2m, 2m+1 (weights after them).
+// Several frames per pass (FP warp groups x FT frames per thread) share the
+// table and the frame-independent work; see the kernel's comment.
 #include <cuda.h>  // CUtensorMap
 #include <stdio.h>
 
