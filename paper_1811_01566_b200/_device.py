@@ -37,11 +37,17 @@ def _staged_h2d(src, device):
     ev = pool["events"][i]
     if ev is not None:
         ev.synchronize()  # the DMA that last read this buffer has finished
-    stage = buf[:nbytes].view(src.dtype).view(src.shape)
-    stage.copy_(src)
+    stage = buf[:nbytes].view(src.dtype)
+    flat = src.reshape(-1)
     out = torch.empty(src.shape, dtype=src.dtype, device=device)
+    oflat = out.view(-1)
+    # chunked: the DMA of chunk i overlaps the host memcpy of chunk i + 1
+    n = flat.numel()
+    step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
     with torch.cuda.device(device):
-        out.copy_(stage, non_blocking=True)
+        for o in range(0, n, step):
+            stage[o:o + step].copy_(flat[o:o + step])
+            oflat[o:o + step].copy_(stage[o:o + step], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
     pool["events"][i] = ev
