@@ -12,4 +12,8 @@ b cfg5 --config cfg5 --steps 5
 b cfg4 --frames 256 --steps 4 --no-e2e
 b cfg2_nearest --interp nearest --steps 20 --no-e2e
 b cfg1_nearest --config cfg1 --interp nearest --steps 20 --no-e2e
-timeout 1200 python -m pytest tests/test_gpu_das.py -q > gpurun_out/pt_das.log 2>&1; tail -2 gpurun_out/pt_das.log
+
+b sta_paper --config sta-paper --steps 10 --no-e2e
+b sta_paper_nearest --config sta-paper --interp nearest --steps 10 --no-e2e
+b pwi_paper --config pwi-paper --steps 20 --no-e2e
+b cfg2_hann_f15 --window hann --f-number 1.5 --steps 20 --no-e2e
