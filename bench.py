@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--frames", type=int, default=32, help="frames per GPU per step")
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--interp", default="linear")
+    ap.add_argument("--split", default="cols", choices=["cols", "rows"],
+                    help="cfg5: split one frame by image columns (rank-local FFT, gather of "
+                         "display tiles) or by depth rows (gather of RF rows, K2 on rank 0)")
     ap.add_argument("--window", default="rectangular", choices=["rectangular", "hann"],
                     help="receive apodisation window (ApodizationSpec)")
     ap.add_argument("--f-number", type=float, default=0.0,
@@ -184,12 +187,18 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
     import paper_1811_01566_b200 as bm
     from paper_1811_01566_b200 import parallel as P
 
-    split = P.LateralSplit(grid, world, rank)
+    rows = args.split == "rows"
+    split = (P.RowSplit if rows else P.LateralSplit)(grid, world, rank)
     eng = bm.BmodeEngine(ctx, split.sub_grid)
     frame = torch.from_numpy(synth_frames(ctx, n_s, 1, 0)).to(dev)  # replicated RF
     _, rf_img, env, peak, status = eng._buffers(1)
 
     def step():
+        if rows:
+            # DAS of this rank's depth band, RF bands gathered, K2 on rank 0
+            eng.plan.beamform_batch(frame, eng.interp, out=rf_img[:1])
+            full = split.gather(rf_img[0]) if world > 1 else rf_img[0]
+            return P.envelope_display(full, eng.range_db)[0] if full is not None else None
         eng.reconstruct(frame)  # DAS + envelope + local peak of this slab
         if world > 1:
             return split.display(env[0], eng.range_db)
@@ -219,9 +228,10 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
             "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic wire phantom + N(0,0.01)",
-            "config": {"workload": "cfg5 STAI 128el x 128tx x 4096 samples -> 2048x2048, lateral "
-                                   "column split, all-reduce(max) + all-gather of display slabs",
-                       "columns_per_rank": split.hi - split.lo},
+            "config": {"workload": "cfg5 STAI 128el x 128tx x 4096 samples -> 2048x2048, " + (
+                "depth-row split, all-gather of RF rows, envelope + display on rank 0" if rows else
+                "lateral column split, all-reduce(max) + all-gather of display slabs"),
+                       ("rows_per_rank" if rows else "columns_per_rank"): split.hi - split.lo},
             "e2e": None, "gpu_launches": 3 * args.steps}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -13,8 +13,15 @@ the CPU tests):
   lane is rank-local.  The only coupling is the per-frame peak of
   dynamic_adjustment (sigproc.py:90): one all-reduce(MAX) of a single
   float, then each rank maps its slab to display values and one gather
-  assembles the B-mode image on the destination rank.  (Splitting by depth
-  rows instead would cut every FFT lane.)
+  assembles the B-mode image on the destination rank.
+
+* **One large frame, split by depth ROWS** (`RowSplit`, the north star's
+  literal "image rows are split across GPUs"): each rank beamforms a band of
+  rows at all columns -- again bitwise the same pixels as one GPU -- but a
+  band cuts every axial FFT lane, so the beamformed RF bands are gathered
+  to the destination rank, which runs the envelope + display of the whole
+  frame (the same kernels as one GPU, so the same bits).  One all-gather of
+  f32 RF rows, no other collective.
 
 The per-rank compute is injectable (`local_fn(sub_grid, rank) -> envelope
 slab`) so the partition/collective logic is testable on CPU with gloo.
@@ -108,3 +115,60 @@ def map_display(env, peak: float, range_db: float):
     db = 20.0 * torch.log10(e[pos] / e.new_tensor(peak))
     out[pos] = torch.clamp(db + range_db, 0.0, range_db) / range_db
     return out
+
+
+def row_bands(n_z: int, world: int) -> list[tuple[int, int]]:
+    """[lo, hi) depth-row ranges, one per rank, sizes differing by <= 1."""
+    return column_slabs(n_z, world)
+
+
+class RowSplit:
+    """Depth-band decomposition of one frame's image grid."""
+
+    def __init__(self, grid, world: int, rank: int):
+        self.grid, self.world, self.rank = grid, int(world), int(rank)
+        self.bands = row_bands(grid.n_z, self.world)
+        lo, hi = self.bands[self.rank]
+        if hi <= lo:
+            raise ValueError(f"rank {rank} has no rows ({grid.n_z} rows, {world} ranks)")
+        self.lo, self.hi = lo, hi
+        self.sub_grid = ImageGrid(np.asarray(grid.x_positions),
+                                  np.asarray(grid.z_positions)[lo:hi])
+
+    def gather(self, band, group=None, dst: int = 0):
+        """Gather equal-padded row bands [rows, n_x] to `dst` and stack them."""
+        import torch
+        import torch.distributed as dist
+
+        h = max(b - a for a, b in self.bands)
+        buf = torch.zeros((h,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
+        buf[: band.shape[0]] = band
+        parts = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(parts, buf.contiguous(), group=group)
+        if dist.get_rank(group) != dst:
+            return None
+        return torch.cat([p[: b - a] for p, (a, b) in zip(parts, self.bands)], dim=0)
+
+
+def envelope_display(rf_img, range_db: float):
+    """Envelope + dB display of one beamformed frame [n_z, n_x] on its device
+    (the bm_envelope_peak + bm_display kernels of the single-GPU chain).
+    Returns (display, envelope)."""
+    import torch
+
+    from . import _native as N
+
+    x = rf_img.contiguous()
+    code = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
+    env = torch.empty_like(x)
+    peak = torch.empty(1, dtype=torch.int32 if code == N.BM_F32 else torch.int64, device=x.device)
+    disp = torch.empty_like(x)
+    status = torch.empty(1, dtype=torch.int32, device=x.device)
+    n_z, n_x = x.shape
+    with torch.cuda.device(x.device):
+        N.call("bm_envelope_peak", code, x.data_ptr(), env.data_ptr(), peak.data_ptr(), 1, n_z, n_x,
+               N.stream_ptr())
+        N.call("bm_display", code, env.data_ptr(), peak.data_ptr(), disp.data_ptr(),
+               status.data_ptr(), 1, n_z * n_x, float(range_db), N.stream_ptr())
+    return disp, env
+

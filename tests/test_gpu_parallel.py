@@ -38,3 +38,28 @@ def test_lateral_slabs_equal_full_frame():
     gpeak = max(peaks)
     disp = torch.cat([P.map_display(e, gpeak, 30.0) for e in env_parts], 1)
     assert torch.equal(disp, disp_full)
+
+
+def test_row_bands_equal_full_frame():
+    """Depth bands of config 5's split by rows, beamformed one after another on
+    one device and stacked: rf bitwise the full frame's; the destination's
+    envelope + display of the stacked frame bitwise the single-GPU chain."""
+    import torch
+
+    ctx, grid, n_s = ME.config_geometry("cfg5", n_z=200, n_x=96)
+    rf = torch.from_numpy(np.random.default_rng(6).normal(size=(128, 128, n_s))
+                          .astype(np.float32)).cuda()
+    full = bm.BmodeEngine(ctx, grid)
+    disp_full = full.reconstruct(rf[None])[0]
+    rf_full = full._buffers(1)[1][0].clone()
+    world = 3
+    bands = []
+    for r in range(world):
+        split = P.RowSplit(grid, world, r)
+        eng = bm.BmodeEngine(ctx, split.sub_grid)
+        eng.reconstruct(rf[None])
+        bands.append(eng._buffers(1)[1][0].clone())
+    stacked = torch.cat(bands, 0)
+    assert torch.equal(stacked, rf_full)
+    disp, _ = P.envelope_display(stacked, 30.0)
+    assert torch.equal(disp, disp_full)

@@ -79,3 +79,44 @@ def test_lateral_split_gloo_matches_single_process(tmp_path, world):
     # display against the all-reduced global peak
     assert np.abs(got["disp"] - disp_ref).max() <= 1e-6
     assert got["disp"].max() == 1.0
+
+
+def _row_worker(rank, world, port, out_path):
+    from oracle import oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx, grid, rf = _geometry()
+        split = P.RowSplit(grid, world, rank)
+        band = O.das_beamform(rf, ctx, split.sub_grid)          # per-rank DAS of a depth band
+        rf_full = split.gather(torch.from_numpy(band))          # the only collective
+        if rank == 0:
+            np.savez(out_path, rf=rf_full.numpy())
+        else:
+            assert rf_full is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_split_gloo_matches_single_process(tmp_path, world):
+    """Depth-band split (RowSplit): the gathered bands are bitwise the
+    single-process beamformed frame, so the destination's envelope + display
+    of it equal the single-GPU chain."""
+    from oracle import oracle as O
+
+    out = str(tmp_path / "rows.npz")
+    mp.spawn(_row_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    got = np.load(out)
+    ctx, grid, rf = _geometry()
+    rf_ref, _, _ = O.bmode_chain(rf, ctx, grid)
+    assert got["rf"].tobytes() == rf_ref.tobytes()
+
+
+def test_row_bands():
+    assert P.row_bands(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    ctx, grid, _ = _geometry()
+    bands = [P.RowSplit(grid, 3, r).sub_grid for r in range(3)]
+    assert sum(b.n_z for b in bands) == grid.n_z
+    assert np.array_equal(np.concatenate([b.z_positions for b in bands]), grid.z_positions)
