@@ -166,7 +166,9 @@ def test_no_contracted_fma_in_das_kernels():
     # {nearest, linear}: FP = 1 x {32, 64}ch, FP = 2 x {16, 32, 64}ch
     # + 16 four-frames-per-thread tma, same apertures, FP = 1 / 2 x {16, 32}ch
     # + 16 of them weighted (Hann / F-number)
-    assert len(das) == 230
+    # + 32 uniform four-frames-per-thread 16ch tma with a compile-time window
+    #   (96 / 128 / 160 / 192 samples) x FP = 1 / 2 x {STA, PW} x {nearest, linear}
+    assert len(das) == 262
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
