@@ -836,6 +836,17 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
 #undef BM_TMA_WI
       k = table7[(fp == 2 ? 16 : 0) + wi * 4 + (lin ? 2 : 0) + (pw ? 1 : 0)];
     }
+    if (W == 96 && !g.uniform && fp == 2 && (!ew || atoi(ew) != 0)) {
+      // weighted (Hann / F-number), 96-sample windows: 16 / 32-channel stages
+#define BM_TMA_WIW(J)                                                                      \
+  das_tma_kernel<false, false, false, true, J, true, 2, 4, 96>,                            \
+      das_tma_kernel<true, false, false, true, J, true, 2, 4, 96>,                         \
+      das_tma_kernel<false, true, false, true, J, true, 2, 4, 96>,                         \
+      das_tma_kernel<true, true, false, true, J, true, 2, 4, 96>
+      static const kfn table8[8] = {BM_TMA_WIW(16), BM_TMA_WIW(32)};
+#undef BM_TMA_WIW
+      k = table8[(tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
+    }
   }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
