@@ -262,14 +262,19 @@ __global__ void display_kernel(const T* __restrict__ e, const typename PeakBits<
   const T pk = PeakBits<T>::value(peak[f]);
   if (blockIdx.x == 0 && threadIdx.x == 0 && status) status[f] = pk > T(0) ? 0 : 1;
   const T r = O::from_double(range_db);
+  // q = e/peak at least 0.1 % below 10^(-R/20) gives 20 log10 q + R < 0 with
+  // a margin far above every rounding of the chain: the clip makes it exactly
+  // 0, so the (f64) log is skipped -- most pixels of a 30 dB display
+  const T q0 = (T)(pow(10.0, -range_db / 20.0) * 0.999);
   const T* ef = e + f * frame_elems;
   T* df = disp + f * frame_elems;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
        i += (int64_t)gridDim.x * blockDim.x) {
     const T v = ef[i];
     T outv = T(0);
-    if (v > T(0) && pk > T(0)) {
-      const T db = O::mul(T(20), log10_rn<T>(O::div(v, pk)));
+    const T q = O::div(v, pk);
+    if (v > T(0) && pk > T(0) && !(q < q0)) {
+      const T db = O::mul(T(20), log10_rn<T>(q));
       T s = O::add(db, r);
       s = s < T(0) ? T(0) : (s > r ? r : s);
       outv = O::div(s, r);
