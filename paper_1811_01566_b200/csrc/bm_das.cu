@@ -17,6 +17,8 @@
 // Thread mapping: one thread per pixel; a CTA owns a 4 x 32 (z x x) tile, a
 // warp owns 32 adjacent lateral pixels of one row, so the gather addresses of
 // a warp for one (e, j) trace fall within a narrow sample window.
+#include <algorithm>
+
 #include "bm_common.cuh"
 
 namespace bm {
@@ -50,16 +52,21 @@ __device__ __forceinline__ T load_or_zero(const T* __restrict__ x, int k, int n)
 // DSMEM: receive delays of the tile cached in shared memory ([n_el][kThreads],
 // each thread owns one column, so no barrier is needed).  Without it (huge
 // apertures) the delay is recomputed per contribution.
-template <typename T, bool PW, bool LINEAR, bool UNIFORM, bool DSMEM>
-__global__ void __launch_bounds__(kThreads) das_kernel(const DasArgs a) {
+//
+// TZ: tile rows (kTileZ by default).  The cached delay table costs
+// n_elements * sizeof(T) bytes per pixel (1 KB for 128 f64 elements), so f64
+// launches take TZ = 1 or 2: more, smaller CTAs per SM, more resident warps.
+template <typename T, bool PW, bool LINEAR, bool UNIFORM, bool DSMEM, int TZ = kTileZ>
+__global__ void __launch_bounds__(TZ * kTileX) das_kernel(const DasArgs a) {
   using O = R<T>;
+  constexpr int kThreads = TZ * kTileX;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* D = reinterpret_cast<T*>(smem_raw);
   const bm_das_geometry& g = a.g;
 
   const int tid = threadIdx.x;
   const int tiles_x = (g.n_x + kTileX - 1) / kTileX;
-  const int iz = (blockIdx.x / tiles_x) * kTileZ + tid / kTileX;
+  const int iz = (blockIdx.x / tiles_x) * TZ + tid / kTileX;
   const int ix = (blockIdx.x % tiles_x) * kTileX + tid % kTileX;
   const bool valid = iz < g.n_z && ix < g.n_x;
   const int izc = min(iz, g.n_z - 1), ixc = min(ix, g.n_x - 1);
@@ -170,12 +177,13 @@ __global__ void span_kernel(const bm_das_geometry g, double f_number, int32_t* s
   }
 }
 
-template <typename T, bool PW, bool LINEAR, bool UNIFORM, bool DSMEM>
+template <typename T, bool PW, bool LINEAR, bool UNIFORM, bool DSMEM, int TZ = kTileZ>
 static int launch_t(const DasArgs& a, int n_frames, cudaStream_t s) {
   const bm_das_geometry& g = a.g;
-  const int tiles = ((g.n_z + kTileZ - 1) / kTileZ) * ((g.n_x + kTileX - 1) / kTileX);
+  constexpr int kThreads = TZ * kTileX;
+  const int tiles = ((g.n_z + TZ - 1) / TZ) * ((g.n_x + kTileX - 1) / kTileX);
   size_t smem = DSMEM ? (size_t)g.n_elements * kThreads * sizeof(T) : 0;
-  auto k = das_kernel<T, PW, LINEAR, UNIFORM, DSMEM>;
+  auto k = das_kernel<T, PW, LINEAR, UNIFORM, DSMEM, TZ>;
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
@@ -188,7 +196,19 @@ static int launch_t(const DasArgs& a, int n_frames, cudaStream_t s) {
 
 template <typename T, bool PW, bool LINEAR, bool UNIFORM>
 static int launch_d(const DasArgs& a, int n_frames, cudaStream_t s) {
-  const size_t smem = (size_t)a.g.n_elements * kThreads * sizeof(T);
+  const size_t per_px = (size_t)a.g.n_elements * sizeof(T);
+  if (sizeof(T) == 8 && per_px * kTileX <= 200 * 1024) {
+    // f64: the TZ (1 or 2 rows of 32 pixels) with the most resident warps
+    // per SM for this table size (227 KB of shared memory per SM)
+    const size_t cap = 227 * 1024;
+    const size_t w1 = std::min<size_t>(cap / (per_px * kTileX + 1024), 32);
+    const size_t w2 = 2 * std::min<size_t>(cap / (per_px * 2 * kTileX + 1024), 16);
+    const char* e = getenv("BM_DAS_GENERIC_TZ");  // A/B override: 1 | 2 | 4
+    const int tz = e ? atoi(e) : (w2 >= w1 ? 2 : 1);
+    if (tz == 1) return launch_t<T, PW, LINEAR, UNIFORM, true, 1>(a, n_frames, s);
+    if (tz == 2) return launch_t<T, PW, LINEAR, UNIFORM, true, 2>(a, n_frames, s);
+  }
+  const size_t smem = per_px * kThreads;
   if (smem <= 200 * 1024) return launch_t<T, PW, LINEAR, UNIFORM, true>(a, n_frames, s);
   return launch_t<T, PW, LINEAR, UNIFORM, false>(a, n_frames, s);
 }
