@@ -58,9 +58,82 @@ __global__ void __launch_bounds__(kFirTile) fir_kernel(const TI* __restrict__ x,
   y[o * n * inner + k * inner + i] = (TO)acc;
 }
 
+// Contiguous lanes (inner == 1): each thread filters kFirR consecutive
+// outputs, so a tap costs one shared-memory load of x for kFirR outputs (the
+// others slide through registers) plus one broadcast load of h[m]: the loop
+// is FP64-pipe bound instead of LSU bound (the one-output kernel above spends
+// 3 wavefronts per output and tap).  The window is padded by one double per
+// 16 so the stride-kFirR lane pattern hits every bank exactly twice.  The
+// sum order per output is the one-output kernel's, bit for bit: the oldest
+// tap first, a product of zero padding before sample 0 adds +-0 to the zero
+// initial state and leaves it +0.
+constexpr int kFirR = 4;
+__host__ __device__ __forceinline__ int fir_pad(int q) { return q + (q >> 4); }
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(kFirTile) fir_rows_kernel(const TI* __restrict__ x,
+                                                            TO* __restrict__ y,
+                                                            const double* __restrict__ taps, int M,
+                                                            int64_t n, int64_t tiles_per_lane) {
+  extern __shared__ double fsm[];
+  double* h = fsm;      // [M]
+  double* w = fsm + M;  // padded [kFirR * kFirTile + M - 1]: x[k0 - (M-1) ..]
+  const int64_t lane = blockIdx.x / tiles_per_lane;
+  const int64_t k0 = (blockIdx.x % tiles_per_lane) * (kFirR * kFirTile);
+  const TI* xl = x + lane * n;
+  for (int m = threadIdx.x; m < M; m += kFirTile) h[m] = taps[m];
+  for (int q = threadIdx.x; q < kFirR * kFirTile + M - 1; q += kFirTile) {
+    const int64_t k = k0 - (M - 1) + q;
+    w[fir_pad(q)] = (k >= 0 && k < n) ? (double)xl[k] : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int64_t kb = k0 + (int64_t)kFirR * t;
+  if (kb >= n) return;
+  // step j handles tap m = M-1-j; xr[r] = x[kb + r - m] = window[kFirR*t + r + j]
+  double xr[kFirR], acc[kFirR];
+#pragma unroll
+  for (int r = 0; r < kFirR; ++r) xr[r] = w[fir_pad(kFirR * t + r)];
+  {
+    const double hm = h[M - 1];
+#pragma unroll
+    for (int r = 0; r < kFirR; ++r) {
+      const double p = __dmul_rn(hm, xr[r]);
+      acc[r] = kb + r >= M - 1 ? p : __dadd_rn(p, 0.0);
+    }
+  }
+  for (int j = 1; j < M; ++j) {
+#pragma unroll
+    for (int r = 0; r < kFirR - 1; ++r) xr[r] = xr[r + 1];
+    xr[kFirR - 1] = w[fir_pad(kFirR * t + kFirR - 1 + j)];
+    const double hm = h[M - 1 - j];
+#pragma unroll
+    for (int r = 0; r < kFirR; ++r) acc[r] = __dadd_rn(__dmul_rn(hm, xr[r]), acc[r]);
+  }
+  TO* yl = y + lane * n;
+#pragma unroll
+  for (int r = 0; r < kFirR; ++r)
+    if (kb + r < n) yl[kb + r] = (TO)acc[r];
+}
+
 template <typename TI, typename TO>
 static int fir_launch(const void* x, void* y, int64_t outer, int64_t n, int64_t inner,
                       const double* taps, int M, cudaStream_t s) {
+  if (inner == 1 && !getenv("BM_FIR_ONE_OUTPUT")) {  // test hook: force the one-output kernel
+    const int win = kFirR * kFirTile + M - 1;
+    const size_t smem = (size_t)(M + fir_pad(win - 1) + 1) * sizeof(double);
+    if (smem <= 200 * 1024) {
+      const int64_t tiles = (n + kFirR * kFirTile - 1) / (kFirR * kFirTile);
+      const int64_t blocks = outer * tiles;
+      if (blocks > 0x7fffffffLL) return BM_ERR_UNSUPPORTED;
+      auto k = fir_rows_kernel<TI, TO>;
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BM_ERR_CUDA;
+      k<<<(unsigned)blocks, kFirTile, smem, s>>>((const TI*)x, (TO*)y, taps, M, n, tiles);
+      return cuda_status();
+    }
+  }
   const size_t smem = (size_t)(2 * M + kFirTile - 1) * sizeof(double);
   if (smem > 200 * 1024) return BM_ERR_UNSUPPORTED;
   const int64_t tiles = (n + kFirTile - 1) / kFirTile;

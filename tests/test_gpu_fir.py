@@ -138,3 +138,26 @@ def test_fir_node_prefilters_frame():
     outputs, timing = bm.execute(graph, (frame, ctx))
     assert outputs["dynamic_adjustment"].stage == "display"
     assert [s for s, _ in timing.stages][0] == "fir"
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("M", [1, 5, 64, 300, 1500])
+def test_fir_row_kernel_bitwise_equals_one_output_kernel(dtype, M, monkeypatch):
+    """Contiguous lanes run the register-blocked kernel (four outputs per
+    thread); it must equal the one-output kernel bit for bit, lengths not a
+    multiple of its 1024-output tile, shorter than the filter, and -0.0
+    products against the zero initial state included."""
+    import torch
+
+    rng = np.random.default_rng(M)
+    h = rng.normal(size=M)
+    h[0] = -abs(h[0])  # a negative newest tap: h*0 = -0.0 at a zero sample
+    for n in (1, 3, 1023, 1025, 2048 + 77):
+        x = rng.normal(size=(5, n)).astype(dtype)
+        x[:, ::7] = 0.0
+        xd = torch.from_numpy(x).cuda()
+        blocked = bm.fir_filter(xd, bm.FirSpec(h)).cpu().numpy()
+        monkeypatch.setenv("BM_FIR_ONE_OUTPUT", "1")
+        one = bm.fir_filter(xd, bm.FirSpec(h)).cpu().numpy()
+        monkeypatch.delenv("BM_FIR_ONE_OUTPUT")
+        assert blocked.tobytes() == one.tobytes(), (M, n)
