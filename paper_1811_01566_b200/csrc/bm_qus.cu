@@ -38,9 +38,18 @@ __global__ void __launch_bounds__(256) moments_kernel(const T* __restrict__ img,
   const int64_t r0 = (w / out_c) * sh, c0 = (w % out_c) * sw;
   const int64_t cnt = (int64_t)wh * ww;
   double s1 = 0, s2 = 0, s3 = 0, k1 = 0, k2 = 0, k3 = 0;
+  // the lane's (row, column) in the window advances by 32 elements per step:
+  // dr rows and dc columns, one carry (no 64-bit division per element)
+  const int dr = 32 / ww, dc = 32 % ww;
+  int qr = lane / ww, qc = lane % ww;
   for (int64_t q = lane; q < cnt; q += 32) {
-    const int64_t r = r0 + q / ww, c = c0 + q % ww;
-    const double x = (double)img[r * n_cols + c];
+    const double x = (double)img[(r0 + qr) * n_cols + c0 + qc];
+    qr += dr;
+    qc += dc;
+    if (qc >= ww) {
+      qc -= ww;
+      ++qr;
+    }
     const double x2 = x * x;
     kahan_add(s1, k1, x);
     kahan_add(s2, k2, x2);
