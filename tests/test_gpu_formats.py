@@ -59,3 +59,25 @@ def test_reconstruct_file_equals_device_reconstruction(tmp_path):
     assert disp.shape == (n,) + grid.shape
     assert torch.equal(disp, ref.cpu())
     assert ctx2.n_tx == ctx.n_tx
+
+
+def test_quantize_vector_and_scalar_paths_equal_numpy():
+    """bm_quantize_u8 on f32: the four-pixels-per-thread path (aligned
+    buffers), its scalar tail and the unaligned scalar path all equal
+    numpy's f32 floor(v * 255 + 0.5), including values on the .5 steps."""
+    import torch
+
+    from paper_1811_01566_b200 import _native as N
+
+    rng = np.random.default_rng(3)
+    steps = (np.arange(256, dtype=np.float32) + np.float32(0.5)) / np.float32(255)
+    for count in (1, 3, 4, 5, 1027, 1 << 16):
+        for off in (0, 1, 3):
+            v = rng.random(count + off, dtype=np.float32)
+            v[off::5] = steps[rng.integers(0, 255, size=len(v[off::5]))]
+            v[off::7] = np.nextafter(v[off::7], np.float32(0))
+            d = torch.from_numpy(v).cuda()[off:]
+            q = torch.empty(count + off, dtype=torch.uint8, device="cuda")[off:]
+            N.call("bm_quantize_u8", N.BM_F32, d.data_ptr(), q.data_ptr(), count, N.stream_ptr())
+            ref = np.floor(v[off:] * np.float32(255) + np.float32(0.5)).astype(np.uint8)
+            assert np.array_equal(q.cpu().numpy(), ref), (count, off)
