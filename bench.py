@@ -14,8 +14,16 @@ GPU > 126 MB L2, so no L2 flush is needed between steps).
 `e2e`:   the same metric through the public engine API from pinned HOST
 buffers, H2D of the RF and D2H of the display inside the timed region.
 
---impl reference: the CPU restatement of the reference (oracle/: C DAS
-kernel + scipy.fft analytic signal + numpy dB) on all host cores, rank 0.
+`roofline`: the DAS kernel against the roof that binds it -- shared-memory
+gathers (8 B per linear contribution at 128 B/clk/SM) or, with one frame per
+thread, the FP32 pipe -- at the SM clock sampled during the run; its HBM
+traffic sits under roofline.hbm.  `stai`: the STAI pipelines (cfg1, cfg3)
+measured in the same run the same way.
+
+--impl reference: the reference itself -- echopipe's own
+pipeline.benchmark (numba DAS on all host cores + scipy.fft + numpy) from
+baseline/_ref, on its own simulator source -- on rank 0, with the C port of
+the same algorithm (oracle/) timed beside it.
 """
 
 from __future__ import annotations
@@ -63,6 +71,10 @@ def parse():
     ap.add_argument("--f-number", type=float, default=0.0,
                     help="dynamic-aperture f-number (0: all elements)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stai", action="store_true",
+                    help="skip the STAI blocks (cfg1 / cfg3) of the default cfg2 run")
+    ap.add_argument("--debug", action="append", default=[],
+                    help="library tuning hook KEY=VALUE (_native.DEBUG_KEYS), e.g. das_ft=2")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -179,9 +191,11 @@ def cpu_reference(ctx, grid, frames, seconds, interp, max_frames=None):
 
 
 def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
-    """BASELINE config 5: one 2048 x 2048 STAI frame per step, image columns
-    split across ranks (parallel.LateralSplit), one all-reduce(MAX) of the
-    peak and one all-gather of display slabs per frame (strong scaling)."""
+    """BASELINE config 5: one 2048 x 2048 STAI frame per step (strong
+    scaling).  Columns: each rank beamforms its column slab, writes
+    [envelope | peak] into its tile, ONE gather to rank 0, rank 0 maps the
+    frame (parallel.LateralSplit).  Rows: each rank beamforms a depth band,
+    ONE gather of the bands, rank 0 runs envelope + display (RowSplit)."""
     import torch
 
     import paper_1811_01566_b200 as bm
@@ -189,26 +203,44 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
 
     rows = args.split == "rows"
     split = (P.RowSplit if rows else P.LateralSplit)(grid, world, rank)
-    eng = bm.BmodeEngine(ctx, split.sub_grid)
+    plan = bm.DasPlan(ctx, split.sub_grid, bm.ApodizationSpec(), np.float32, ctx.n_elements)
     frame = torch.from_numpy(synth_frames(ctx, n_s, 1, 0)).to(dev)  # replicated RF
-    _, rf_img, env, peak, status = eng._buffers(1)
+    f32 = torch.float32
+    launches = [0]
+    if rows:
+        send = split.send_band(f32, dev)
+        recv = split.recv_bands(f32, dev) if rank == 0 else None
+        mine = send[None, : split.hi - split.lo]
 
-    def step():
-        if rows:
-            # DAS of this rank's depth band, RF bands gathered, K2 on rank 0
-            eng.plan.beamform_batch(frame, eng.interp, out=rf_img[:1])
-            full = split.gather(rf_img[0]) if world > 1 else rf_img[0]
-            return P.envelope_display(full, eng.range_db)[0] if full is not None else None
-        eng.reconstruct(frame)  # DAS + envelope + local peak of this slab
-        if world > 1:
-            return split.display(env[0], eng.range_db)
-        return P.map_display(env[0], float(env[0].max()), eng.range_db)
+        def step():
+            plan.beamform_batch(frame, out=mine)
+            full = split.gather(send, recv) if world > 1 else send
+            launches[0] += 1
+            if full is not None:
+                launches[0] += 1
+                return P.envelope_display(full, 30.0)
+    else:
+        tile = split.send_tile(f32, dev)
+        recv = split.recv_tiles(f32, dev) if rank == 0 else None
+        slab = torch.empty((1,) + plan.shape, dtype=f32, device=dev)
+
+        def step():
+            plan.beamform_batch(frame, out=slab)
+            split.envelope_into_tile(slab[0], tile)
+            got = split.gather(tile, recv) if world > 1 else tile[None]
+            launches[0] += 2
+            if got is not None:
+                launches[0] += 1
+                return split.display(got, 30.0)
 
     for _ in range(args.warmup):
-        step()
+        res = step()
     torch.cuda.synchronize()
+    if res is not None and int(res[1].item()) != 0:
+        raise bm.AllZeroInput("dynamic adjustment needs a strictly positive element")
     if world > 1:
         torch.distributed.barrier()
+    launches[0] = 0
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
@@ -229,12 +261,243 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic wire phantom + N(0,0.01)",
             "config": {"workload": "cfg5 STAI 128el x 128tx x 4096 samples -> 2048x2048, " + (
-                "depth-row split, all-gather of RF rows, envelope + display on rank 0" if rows else
-                "lateral column split, all-reduce(max) + all-gather of display slabs"),
+                "depth-row split, one gather of RF bands, envelope + display on rank 0" if rows
+                else "lateral column split, one gather of [envelope | peak] tiles, display on "
+                     "rank 0"),
                        ("rows_per_rank" if rows else "columns_per_rank"): split.hi - split.lo},
-            "e2e": None, "gpu_launches": 3 * args.steps}), flush=True)
+            "e2e": None, "gpu_launches": launches[0]}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def das_roofline(eng, ctx, grid, n_s, B, das_ms, interp, clk, n_sm, peaks, workload):
+    """Roofline of one DAS launch of B frames, measured
+    peaks from profiles/r01_microbench.json at the SM clock sampled in the run:
+      * shared-memory gathers: 8 B per linear contribution (4 nearest); LDS.32
+        retires one warp instruction (128 B) per clk per SM;
+      * FP32 pipe: 5/FT + 4 lane-ops per linear contribution (3/FT + 1
+        nearest; +2 per (pixel, channel) and +... with weights) at 128
+        lane-ops/clk/SM, FT = frames per thread of the launch shape.
+    The binding one is the larger time; HBM (RF + image bytes) is ~50x away
+    and reported under "hbm" with the ncu DRAM traffic."""
+    import torch
+
+    n_rx = ctx.rx_channel_map.shape[1] if ctx.rx_channel_map is not None else ctx.n_elements
+    contrib = B * ctx.n_tx * n_rx * grid.n_z * grid.n_x
+    span = eng.plan._bufs.get("span")
+    if span is not None and eng.plan._geom.rx_identity:
+        # F-number gate: terms outside a pixel's active span have weight 0 and
+        # are exact zeros the kernel skips -- the algorithmic work is the
+        # active contributions
+        sp = span.view(-1, 2).to(torch.int64)
+        lo, hi = sp[:, 0].clamp(min=0), sp[:, 1].clamp(max=ctx.n_elements - 1)
+        contrib = int(B * ctx.n_tx * (hi - lo + 1).clamp(min=0).sum().item())
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    shape = eng.plan.launch_shape(n_s, B, interp) or {"ft": 1, "fp": 1}
+    ft = shape["ft"]
+    if eng.plan.uniform:
+        ops = (5.0 / ft + 4.0) if interp == "linear" else (3.0 / ft + 1.0)
+    else:
+        ops = (7.0 / ft + 4.0) if interp == "linear" else (3.0 / ft + 2.0)
+    gb = 8 if interp == "linear" else 4
+    clk_hz = sm_mhz * 1e6
+    t_fp32 = contrib * ops / (n_sm * 128 * clk_hz)
+    t_lds = contrib * gb / (n_sm * 128 * clk_hz)
+    t = das_ms / 1000.0
+    frame_bytes = ctx.n_tx * n_rx * n_s * 4
+    img_bytes = grid.n_z * grid.n_x * 4
+    hbm_bytes = B * (frame_bytes + img_bytes)
+    hbm_peak = peaks.get("hbm_gbs", 6450.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "das_traffic.json")))
+        if prof.get("workload") == workload and prof.get("interp") == interp:
+            traffic = round(prof["dram_bytes_per_frame"] * B, 0)
+    except Exception:
+        pass
+    if t_lds >= t_fp32:
+        bound, achieved = "smem_gather", contrib * gb / t / 1e9
+        peak, unit = n_sm * 128 * clk_hz / 1e9, "GB/s"
+        per = f"{gb} B gathered per contribution"
+    else:
+        bound, achieved = "fp32", contrib * ops / t / 1e12
+        peak, unit = n_sm * 128 * clk_hz / 1e12, "TFLOP/s"
+        per = f"{ops:.4g} FP32 lane-ops per contribution"
+    return {
+        "bound": bound, "achieved": round(achieved, 1 if unit == "GB/s" else 3),
+        "peak": round(peak, 1 if unit == "GB/s" else 3), "unit": unit,
+        "frac": round(max(t_fp32, t_lds) / t, 4), "traffic": traffic,
+        "kernel": f"bm_das_beamform ({eng.plan.kernel_for(n_s, interp)})",
+        "kernel_ms_per_launch": round(das_ms, 4),
+        "algorithmic": f"{contrib} contributions per launch x {per}",
+        "peak_source": ("measured per-SM rates (profiles/r01_microbench.json: LDS.32 1 warp-instr/"
+                        "clk/SM, FADD2/FFMA2 128 lane-ops/clk/SM) x %d SMs x %.0f MHz sampled "
+                        "during the run" % (n_sm, sm_mhz)),
+        "launch_shape": shape,
+        "t_smem_gather_roof_ms": round(t_lds * 1000, 4),
+        "t_fp32_roof_ms": round(t_fp32 * 1000, 4),
+        "fp32_lane_ops_per_contribution": round(ops, 4),
+        "hbm": {"achieved": round(hbm_bytes / t / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_bytes / t / 1e9 / hbm_peak, 4),
+                "algorithmic_bytes_per_launch": hbm_bytes,
+                "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else
+                "fallback"},
+    }
+
+
+def time_engine(eng, rf, out, steps, warmup, barrier, max_over_ranks):
+    """Device-resident steps of eng.reconstruct: (ms total, mean DAS ms per
+    launch, launches).  DAS is bracketed by events on its own stream."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        eng.reconstruct(rf, out=out)
+    torch.cuda.synchronize()
+    eng.check()
+    das_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+    launches0 = eng.launches
+    barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for k in range(steps):
+        eng.reconstruct(rf, out=out, stream=stream, das_events=das_ev[k])
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    eng.check()
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end))
+    das_ms = statistics.mean(a.elapsed_time(b) for a, b in das_ev)
+    return ms_total, das_ms, eng.launches - launches0
+
+
+def stai_block(name, B, args, dev, clocks_fn, n_sm, peaks, barrier, max_over_ranks):
+    """A STAI pipeline measured in the same run as the headline (BASELINE's
+    metric names both the STAI and the PWI pipelines)."""
+    import torch
+
+    import paper_1811_01566_b200 as bm
+    from paper_1811_01566_b200 import environment as ME
+
+    ctx, grid, n_s = ME.config_geometry(name)
+    distinct = min(B, 4)
+    host = synth_frames(ctx, n_s, distinct, 0)
+    rf = torch.from_numpy(host).to(dev)
+    if distinct < B:  # inputs still exceed L2 (B x 33.5 / 268 MB)
+        rf = rf.repeat((B + distinct - 1) // distinct, 1, 1, 1)[:B].contiguous()
+    eng = bm.BmodeEngine(ctx, grid, interp=args.interp)
+    out = torch.empty((B, grid.n_z, grid.n_x), dtype=torch.float32, device=dev)
+    steps = max(5, args.steps // 2) if name != "cfg1" else args.steps
+    ms, das_ms, launches = time_engine(eng, rf, out, steps, args.warmup, barrier, max_over_ranks)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    clk = clocks_fn()
+    rl = das_roofline(eng, ctx, grid, n_s, B, das_ms, args.interp, clk, n_sm, peaks,
+                      WORKLOADS[name])
+    del rf, out
+    torch.cuda.empty_cache()
+    return {"workload": WORKLOADS[name].replace("linear", args.interp), "value": round(
+        world * B * steps / (ms / 1000.0), 2), "unit": "frames/s",
+        "frames_per_gpu_per_step": B, "steps": steps, "ms_per_step": round(ms / steps, 4),
+        "das_ms_per_frame": round(das_ms / B, 5),
+        "envelope_display_ms_per_frame": round((ms / steps - das_ms) / B, 5),
+        "binding": {k: rl[k] for k in ("bound", "achieved", "peak", "unit", "frac",
+                                       "launch_shape", "kernel_ms_per_launch")},
+        "gpu_launches": launches}
+
+
+def reference_arm(args, ctx, grid, n_s, world):
+    """--impl reference: echopipe itself (baseline/_ref, its own
+    pipeline.benchmark on its own SimulatorSource, numba threads = all host
+    cores), the C port of the same algorithm timed beside it."""
+    frames = synth_frames(ctx, n_s, 2, 0)
+    port = []
+    for i in range(args.warmup + args.steps):
+        fps, cores, n, el = cpu_reference(ctx, grid, frames, 0.0, args.interp, max_frames=1)
+        if i >= args.warmup:
+            port.append(el / n)
+    port_ms = statistics.median(port) * 1000.0
+    ref = None
+    try:
+        ref = echopipe_benchmark(args, grid, n_s, args.steps, args.warmup)
+    except Exception as exc:  # pragma: no cover - reported, not hidden
+        ref = {"error": f"{type(exc).__name__}: {exc}"}
+    sample = f"1 {args.config} frame per step"
+    if ref is not None and "ms" in ref:
+        ms, kind, cores = ref["ms"], "reference", ref["threads"]
+        what = (f"{sample}: echopipe {ref['version']} pipeline.benchmark (numba _das_kernel on "
+                f"{ref['threads']} threads, effective parallelism {ref['effective']} pixel blocks "
+                f"of 16384; scipy.fft; numpy), median of {args.steps} frames after "
+                f"{args.warmup} warm-up, plan cached")
+    else:
+        ms, kind, cores = port_ms, "port", cores
+        what = f"{sample}: oracle/ C DAS (pthreads, all cores) + scipy.fft analytic + numpy dB"
+    val = 1000.0 / ms
+    line = {
+        "impl": "reference", "metric": "B-mode frames/sec", "value": round(val, 4),
+        "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic wire phantom + N(0,0.01)",
+        "config": {"workload": WORKLOAD, "frames_per_step": 1},
+        "cpu_baseline": {"value": round(val, 4), "unit": "frames/s", "cores": cores, "kind": kind,
+                         "sample": what},
+        "e2e": {"value": round(val, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "port": {"value": round(1000.0 / port_ms, 4), "unit": "frames/s", "cores": cores,
+                 "kind": "port", "ms_per_frame": round(port_ms, 3),
+                 "sample": "oracle/ C DAS (pthreads, all cores) + scipy.fft + numpy dB, same "
+                           "frames, plan prebuilt"},
+    }
+    if ref is not None and "stages_ms" in ref:
+        line["reference_stages_ms"] = ref["stages_ms"]
+    if ref is not None and "error" in ref:
+        line["reference_error"] = ref["error"]
+    print(json.dumps(line), flush=True)
+
+
+def echopipe_benchmark(args, grid_m, n_s, steps, warmup):
+    """echopipe's own benchmark (pipeline.py:398-437) of its bmode_chain on
+    its own seeded simulator (environment.py:181-221), imported from the
+    vendored install baseline/_ref."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "echopipe")):
+        raise FileNotFoundError("baseline/_ref/echopipe not installed")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_echopipe")
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import numba
+    from echopipe import __version__ as ver  # noqa: F401
+    from echopipe import environment as EE
+    from echopipe import pipeline as EPL
+    from echopipe import presets as EPR
+    from echopipe import types as ET
+
+    from paper_1811_01566_b200 import environment as ME
+
+    ctx_m, _, _ = ME.config_geometry(args.config)
+    if ctx_m.is_pw:
+        scheme = ET.PwScheme(ctx_m.tx_scheme.angles_rad)
+    else:
+        scheme = ET.StaScheme(ctx_m.tx_scheme.tx_elements)
+    ctx = ET.AcquisitionContext(ctx_m.speed_of_sound, ctx_m.sampling_frequency,
+                                ctx_m.n_elements, ctx_m.pitch, scheme,
+                                rx_channel_map=ctx_m.rx_channel_map)
+    threads = os.cpu_count() or 1
+    numba.set_num_threads(min(threads, numba.config.NUMBA_NUM_THREADS))
+    spec = EPL.bmode_chain(interpolation=args.interp,
+                           grid={"x_positions": grid_m.x_positions.tolist(),
+                                 "z_positions": grid_m.z_positions.tolist()})
+    graph = EPL.build_graph(spec)
+    env = EE.open_simulator(EPR.wire_phantom(), ctx, n_s, dtype=np.float32, seed=0,
+                            noise_std=0.01)
+    res = EPL.benchmark(graph, env, n_frames=steps, warmup=max(1, warmup))
+    n_px = grid_m.n_z * grid_m.n_x
+    return {"ms": res.timing.total_ms, "threads": numba.get_num_threads(),
+            "effective": min(numba.get_num_threads(), -(-n_px // 16384)),
+            "version": getattr(sys.modules["echopipe"], "__version__", "?"),
+            "stages_ms": {k: round(v, 3) for k, v in res.timing.stages}}
 
 
 def main():
@@ -254,32 +517,17 @@ def main():
     img_bytes = grid.n_z * grid.n_x * 4
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        frames = synth_frames(ctx, n_s, 2, 0)
-        times = []
-        for i in range(args.warmup + args.steps):
-            fps, cores, n, el = cpu_reference(ctx, grid, frames, 0.0, args.interp, max_frames=1)
-            if i >= args.warmup:
-                times.append(el / n)
-        ms = statistics.median(times) * 1000.0
-        val = 1000.0 / ms
-        print(json.dumps({
-            "impl": "reference", "metric": "B-mode frames/sec", "value": round(val, 4),
-            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic wire phantom + N(0,0.01)",
-            "config": {"workload": WORKLOAD, "frames_per_step": 1},
-            "cpu_baseline": {"value": round(val, 4), "unit": "frames/s", "cores": cores,
-                             "kind": "port",
-                             "sample": f"1 {args.config} frame per step: oracle/ C DAS (pthreads, all "
-                                       "cores) + scipy.fft analytic + numpy dB"},
-            "e2e": {"value": round(val, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}), flush=True)
+        if rank == 0:
+            reference_arm(args, ctx, grid, n_s, world)
         return
 
     import torch
 
+    from paper_1811_01566_b200 import _native as N
+
+    for kv in args.debug:
+        k, v = kv.split("=")
+        N.load().bm_debug_set(N.DEBUG_KEYS[k], int(v))
     if world > 1:
         import torch.distributed as dist
 
@@ -300,7 +548,12 @@ def main():
         WORKLOAD = WORKLOAD + f", {args.window} F={args.f_number:g}"
     rf = torch.from_numpy(host).to(dev)
     out = torch.empty((B, grid.n_z, grid.n_x), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
 
     def barrier():
         if world > 1:
@@ -319,26 +572,10 @@ def main():
     for _ in range(args.warmup):
         eng.reconstruct(rf, out=out)
     torch.cuda.synchronize()
-    eng.check()
-    das_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
     clocks.mark()  # keep only samples taken from here on
-    launches0 = eng.launches
-    barrier()
-    torch.cuda.synchronize()
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_start.record()
-    for k in range(args.steps):
-        # the DAS launch is bracketed by events on its own stream, for the roofline
-        eng.reconstruct(rf, out=out, stream=stream, das_events=das_ev[k])
-    t_end.record()
-    torch.cuda.synchronize()
-    barrier()
+    ms_total, das_ms, launches = time_engine(eng, rf, out, args.steps, 0, barrier, max_over_ranks)
     clk = clocks.stop()
-    launches = eng.launches - launches0
-    ms_total = max_over_ranks(t_start.elapsed_time(t_end))
     ms_step = ms_total / args.steps
-    das_ms = statistics.mean(a.elapsed_time(b) for a, b in das_ev)
     value = world * B * args.steps / (ms_total / 1000.0)
 
     # ---- end-to-end through the public API from pinned host memory ----------
@@ -351,8 +588,8 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        # every step: H2D of its 32 RF frames from pinned host memory, the
-        # chain, D2H of its 32 displays; steps are pipelined back to back and
+        # every step: H2D of its B RF frames from pinned host memory, the
+        # chain, D2H of its B displays; steps are pipelined back to back and
         # the clock stops when the last display is on the host
         eng.reconstruct_host_stream([(rf_h, disp_h)] * e2e_steps)
         el = max_over_ranks(time.perf_counter() - t0)
@@ -360,6 +597,24 @@ def main():
         e2e = {"value": round(world * B * e2e_steps / el, 2), "unit": "frames/s",
                "h2d_bytes_per_step": B * frame_bytes, "d2h_bytes_per_step": B * img_bytes,
                "ms_per_step": round(el / e2e_steps * 1000.0, 3)}
+        del rf_h, disp_h
+
+    roofline = das_roofline(eng, ctx, grid, n_s, B, das_ms, args.interp, clk, n_sm, peaks,
+                            WORKLOAD)
+
+    stai = None
+    if not args.no_stai and args.config == "cfg2":
+        del rf
+        torch.cuda.empty_cache()
+        clocks2 = ClockSampler(local)
+        clocks2.start()
+        clocks2.mark()
+        stai = {}
+        for name, nb in (("cfg1", 32), ("cfg3", 8)):
+            stai[name] = stai_block(name, nb, args, dev, lambda: dict(clk), n_sm, peaks, barrier,
+                                    max_over_ranks)
+        clk2 = clocks2.stop()
+        stai["clocks"] = clk2
 
     if rank != 0:
         if world > 1:
@@ -371,86 +626,12 @@ def main():
                               "(numpy in, numpy display out, pageable copies); value above is "
                               "the batched engine from pinned memory")
 
-    # ---- roofline of the dominant kernel (DAS) ------------------------------
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    das_bytes = B * (frame_bytes + img_bytes)  # algorithmic HBM bytes per launch
-    achieved = das_bytes / (das_ms / 1000.0) / 1e9
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "das_traffic.json")))
-        if prof.get("workload") == WORKLOAD and prof.get("interp") == args.interp:
-            traffic = prof["dram_bytes_per_frame"] * B
-    except Exception:
-        pass
-    contrib = B * ctx.n_tx * n_rx * grid.n_z * grid.n_x
-    span = eng.plan._bufs.get("span")
-    if span is not None and eng.plan._geom.rx_identity:
-        # F-number gate: terms outside a pixel's active span have weight 0 and
-        # are exact zeros the kernel may skip, so the algorithmic work is the
-        # active contributions (identity / contiguous maps: the span clipped
-        # to the elements each transmit records)
-        sp = span.view(-1, 2).to(torch.int64)
-        lo, hi = sp[:, 0].clamp(min=0), sp[:, 1].clamp(max=ctx.n_elements - 1)
-        contrib = int(B * ctx.n_tx * (hi - lo + 1).clamp(min=0).sum().item())
-    sm_mhz = clk["sm_mhz"] or 1965.0
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Rooflines of DAS, both measured on this B200
-    # (profiles/r01_microbench.json):
-    #  * FP32 pipe: the exact (bitwise) linear formulation is 9 FP32 lane-ops
-    #    per contribution (t, floor, k0, a, 1-a, 2 rounded products, 2 adds;
-    #    nearest: 4); FADD2/FFMA2 retire 2 warp-instr/clk/SM = 128 lane-ops.
-    #  * shared-memory gathers: 2 x 4 B per linear contribution (1 nearest);
-    #    LDS.32 retires 1 warp-instr/clk/SM = 128 B/clk/SM.
-    # The binding roof is the slower of the two; HBM is ~100x away.
-    #  * a thread that accumulates ft frames (bm_das_launch_shape) computes the
-    #    frame-independent part once per (pixel, channel): linear 5 lane-ops
-    #    (t, floor, k0, a, 1-a) + 4 per frame, nearest 3 (t, +0.5, floor) + 1.
-    shape = eng.plan.launch_shape(n_s, B, args.interp) or {"ft": 1}
-    ft = shape["ft"]
-    #    Non-uniform apodisation adds w*(1-a), w*a per (pixel, channel)
-    #    (linear) or one w*x per frame (nearest).
-    if eng.plan.uniform:
-        ops = (5.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 1.0)
-    else:
-        ops = (7.0 / ft + 4.0) if args.interp == "linear" else (3.0 / ft + 2.0)
-    gb = 8 if args.interp == "linear" else 4
-    t_fp32 = contrib * ops / (n_sm * 128 * sm_mhz * 1e6)
-    t_lds = contrib * gb / (n_sm * 128 * sm_mhz * 1e6)
-    roofline = {
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-        "kernel": f"bm_das_beamform ({eng.plan.kernel_for(n_s, args.interp)})",
-        "kernel_ms_per_launch": round(das_ms, 4),
-        "algorithmic_bytes_per_launch": das_bytes,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-        "note": "DAS is bound on chip (SMEM gathers / FP32 pipe), not by HBM: see binding",
-        "binding": {
-            "resource": ("max of: SMEM gather roof (%d B per contribution, 128 B/clk/SM) and "
-                         "FP32 pipe (%.4g lane-ops per contribution at %d frame(s) per thread, "
-                         "128 lane-ops/clk/SM)" % (gb, ops, ft)),
-            "bound_by": "smem_gather" if t_lds >= t_fp32 else "fp32",
-            "launch_shape": shape,
-            "contributions_per_launch": contrib,
-            "achieved_gcontrib_s": round(contrib / (das_ms / 1000.0) / 1e9, 1),
-            "achieved_tflops_fp32_lane_ops": round(contrib * ops / (das_ms / 1000.0) / 1e12, 2),
-            "peak_tflops_fp32_lane_ops": round(n_sm * 128 * sm_mhz * 1e6 / 1e12, 2),
-            "t_fp32_roof_ms": round(t_fp32 * 1000, 4),
-            "t_smem_gather_roof_ms": round(t_lds * 1000, 4),
-            "frac": round(max(t_fp32, t_lds) / (das_ms / 1000.0), 4),
-            "sm_mhz": sm_mhz, "n_sm": n_sm},
-    }
-
     cpu = None
     if not args.no_cpu and args.cpu_seconds > 0 and world == 1:  # rank 0 at N=1 only
         fps, cores, n, el = cpu_reference(ctx, grid, host[:4], args.cpu_seconds, args.interp)
         cpu = {"value": round(fps, 4), "unit": "frames/s", "cores": cores, "kind": "port",
-               "sample": f"{n} {args.config} frames in {el:.1f}s: oracle/ C DAS (pthreads) + scipy.fft "
-                         f"+ numpy dB, plan prebuilt"}
+               "sample": f"{n} {args.config} frames in {el:.1f}s: oracle/ C DAS (pthreads) + "
+                         f"scipy.fft + numpy dB, plan prebuilt"}
 
     line = {
         "metric": "B-mode frames/sec", "value": round(value, 2), "unit": "frames/s",
@@ -463,7 +644,8 @@ def main():
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
         "cpu_baseline": cpu,
         "stages_ms_per_frame": {"das": round(das_ms / B, 5),
-                                "envelope+dB": round((ms_step - das_ms) / B, 5)},
+                                "envelope+dB (fused)": round((ms_step - das_ms) / B, 5)},
+        "stai": stai,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -20,6 +20,8 @@
  *   bm_dynamic_adjustment  <- dynamic_adjustment sigproc.py:81-97
  *   bm_envelope_peak       <- analytic_signal + envelope + the `e.max()` of
  *                             dynamic_adjustment (sigproc.py:48-90), fused
+ *   bm_envelope_display    <- analytic_signal + envelope + dynamic_adjustment
+ *                             (sigproc.py:48-97), one fused launch
  *   bm_display             <- the mapping half of dynamic_adjustment
  *                             (sigproc.py:91-97) given the peak
  *   bm_fir_filter          <- fir_filter sigproc.py:36-45 (operator
@@ -39,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BMODE200_ABI_VERSION 2
+#define BMODE200_ABI_VERSION 3
 
 /* element type of every floating-point buffer of one call */
 enum { BM_F32 = 0, BM_F64 = 1 };
@@ -147,10 +149,27 @@ int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_stride, int32
 int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
                     void* out, int64_t out_frame_stride, int32_t n_frames, void* stream);
 
+/* K2 workspace: bytes of caller-owned DEVICE scratch the sigproc op `op`
+ * needs for this shape (0 when its lanes fit on chip).  op: 0 analytic signal,
+ * 1 envelope + peak, 2 envelope + display.  Lanes of length n run along the
+ * middle axis of [outer][n][inner]; for images, outer = frames, n = n_z,
+ * inner = n_x.  Host only (reads the device's occupancy limits). */
+int64_t bm_sigproc_ws_bytes(int32_t op, int32_t dtype, int64_t outer, int64_t n, int64_t inner);
+
+/* Trace padding for bm_das_beamform: n_traces traces of n_samples samples
+ * (row pitch src_pitch elements) copied into rows of dst_samples, the tail
+ * zeroed (the TMA kernel needs rows that are a multiple of 16 bytes; zeros
+ * past the trace are exactly what the reference's sentinels contribute).
+ * Device pointers, stream-ordered DMA, no kernel. */
+int bm_pad_traces(int32_t dtype, const void* src, int64_t src_pitch, int64_t n_traces,
+                  int64_t n_samples, void* dst, int64_t dst_samples, void* stream);
+
 /* Analytic signal along the middle axis of a contiguous [outer, n, inner]
- * real array x; z is complex interleaved (re, im) of the same dtype. */
+ * real array x; z is complex interleaved (re, im) of the same dtype.  Any
+ * n >= 2 (mixed radix, Bluestein for prime factors > 61): ws / ws_bytes as
+ * bm_sigproc_ws_bytes(0, ...) says (may be NULL / 0 when that is 0). */
 int bm_analytic_signal(int32_t dtype, const void* x, void* z, int64_t outer, int64_t n,
-                       int64_t inner, void* stream);
+                       int64_t inner, void* ws, int64_t ws_bytes, void* stream);
 
 /* e[i] = |z[i]| for `count` complex elements. */
 int bm_envelope(int32_t dtype, const void* z, void* e, int64_t count, void* stream);
@@ -158,9 +177,24 @@ int bm_envelope(int32_t dtype, const void* z, void* e, int64_t count, void* stre
 /* Fused analytic -> |.| -> per-frame max, along axis 0 of n_frames images
  * [n_z, n_x] (frame f at rf_img + f*n_z*n_x).  env receives the envelope;
  * peak receives, per frame, the max envelope as raw IEEE bits
- * (uint32 for BM_F32, uint64 for BM_F64).  peak is reset by this call. */
+ * (uint32 for BM_F32, uint64 for BM_F64; NaN wins).  peak is reset by this
+ * call.  ws: bm_sigproc_ws_bytes(1, ...). */
 int bm_envelope_peak(int32_t dtype, const void* rf_img, void* env, void* peak,
-                     int32_t n_frames, int64_t n_z, int64_t n_x, void* stream);
+                     int32_t n_frames, int64_t n_z, int64_t n_x, void* ws, int64_t ws_bytes,
+                     void* stream);
+
+/* K2 + K3 in one launch: analytic -> |.| -> per-frame max -> display
+ * (sigproc.py:48-97) over n_frames images, the envelope kept on chip (a
+ * persistent cooperative kernel; frames whose shape it cannot hold run
+ * bm_envelope_peak into disp and the display mapping in place).  disp, peak
+ * and status as bm_envelope_peak / bm_display.  ws: bm_sigproc_ws_bytes(2,
+ * ...), never 0 (per-frame completion counters). */
+int bm_envelope_display(int32_t dtype, const void* rf_img, void* disp, void* peak,
+                        int32_t* status, int32_t n_frames, int64_t n_z, int64_t n_x,
+                        double range_db, void* ws, int64_t ws_bytes, void* stream);
+
+/* e[i] = |x[i]| for `count` real elements (envelope of a real input, np.abs). */
+int bm_abs(int32_t dtype, const void* x, void* e, int64_t count, void* stream);
 
 /* Per-frame max of `frame_elems` non-negative values (same peak encoding). */
 int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
@@ -171,6 +205,16 @@ int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
  * sigproc.py:91-92), else 0.  disp has the dtype of e. */
 int bm_display(int32_t dtype, const void* e, const void* peak, void* disp, int32_t* status,
                int32_t n_frames, int64_t frame_elems, double range_db, void* stream);
+
+/* Display of one frame split laterally over n_tiles ranks:
+ * tile t starts at tiles + t*tile_stride and holds the envelope of its column
+ * slab as [n_z][w_t] followed, in its LAST element, by the slab's peak bits
+ * (bm_envelope_peak's encoding); slabs follow an even split of n_x (the first
+ * n_x % n_tiles one column wider).  disp [n_z][n_x] is mapped with the max of
+ * the tiles' peaks; *status = 1 if that is not > 0 (AllZeroInput). */
+int bm_display_tiles(int32_t dtype, const void* tiles, int32_t n_tiles, int64_t tile_stride,
+                     int64_t n_z, int64_t n_x, void* disp, int32_t* status, double range_db,
+                     void* stream);
 
 /* dynamic_adjustment as one call: bm_frame_peak then bm_display. */
 int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
@@ -212,6 +256,29 @@ int bm_simulate_rf(int32_t scheme, int32_t n_tx, int32_t n_rx, int32_t n_samples
                    const double* sin_a, const int32_t* rx_map, const double* t0, double c,
                    double fs, double center_frequency, double n_cycles, const double* scatterers,
                    int32_t n_scatterers, int32_t out_dtype, void* out, void* stream);
+
+/* Test and tuning hooks: process-wide, thread-safe integers, 0 = default.
+ * They select which kernel / launch shape runs (every variant computes the
+ * same bits or the same tolerance class); production callers never set them.
+ * The library reads no environment variables. */
+enum {
+  BM_DBG_DAS_KERNEL = 0,       /* 1: never the TMA kernel (generic kernel)           */
+  BM_DBG_DAS_FP = 1,           /* TMA: consumer warp groups per delay table (1 | 2)  */
+  BM_DBG_DAS_FT = 2,           /* TMA: frames per thread (1 | 2 | 4)                 */
+  BM_DBG_DAS_FPC = 3,          /* TMA: frames per CTA                                */
+  BM_DBG_DAS_TJC = 4,          /* TMA: receive channels per stage (32 | 64 | 128)    */
+  BM_DBG_DAS_RUNTIME_W = 5,    /* TMA: 1 = runtime window width kernels              */
+  BM_DBG_DAS_TILE = 6,         /* bm_das_prepare: tile shape 1..4 (contiguous maps)  */
+  BM_DBG_DAS_VERBOSE = 7,      /* TMA: print the launch shape to stderr              */
+  BM_DBG_DAS_GENERIC_TZ = 8,   /* generic kernel, f64: tile rows 1 | 2 | 4           */
+  BM_DBG_FFT_PATH = 9,         /* analytic signal: 1 lane kernel, 2 global stages,
+                                  3 Bluestein (0: register kernel where it applies)  */
+  BM_DBG_NO_FUSED_DISPLAY = 10,/* bm_envelope_display: envelope + display launches  */
+  BM_DBG_FIR_ONE_OUTPUT = 11,  /* FIR: one output per thread kernel                  */
+  BM_DBG_COUNT = 12
+};
+int bm_debug_set(int32_t key, int32_t value); /* returns the previous value     */
+int bm_debug_get(int32_t key);
 
 const char* bm_error_string(int code);
 int bm_abi_version(void);

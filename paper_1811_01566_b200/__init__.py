@@ -7,11 +7,13 @@ sm_100a CUDA kernels in ``_lib/libbmode200.so`` (C ABI: include/bmode200.h).
 Public names mirror echopipe/__init__.py:9-64 for the path.
 """
 
-from .beamform import INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform
+from .beamform import (INTERPOLATION_MODES, DasPlan, active_aperture, das_beamform,
+                       das_beamform_oracle)
 from . import engine, parallel, qus
 from .engine import BmodeEngine
 from .environment import (DatasetSource, Environment, Phantom, SimulatorSource,
-                          default_pw_angles, open_dataset, open_simulator, simulate_rf,
+                          default_pw_angles, next_observation, open_dataset, open_simulator,
+                          simulate_rf,
                           simulate_rf_device, wire_phantom)
 from .formats import WfrfReader, read_wfrf, write_pgm, write_wfrf
 from .errors import (AllZeroInput, AxisTooShort, DimensionMismatch, EchopipeError,

@@ -20,6 +20,15 @@ BM_STA, BM_PW = 0, 1
 BM_NEAREST, BM_LINEAR = 0, 1
 BM_RECTANGULAR, BM_HANN = 0, 1
 BM_ERR_AXIS_TOO_SHORT = 4
+ABI_VERSION = 3
+
+# bm_sigproc_ws_bytes ops
+SIG_ANALYTIC, SIG_ENVELOPE_PEAK, SIG_ENVELOPE_DISPLAY = 0, 1, 2
+
+# test / tuning hooks (include/bmode200.h BM_DBG_*): name -> key
+DEBUG_KEYS = {"das_kernel": 0, "das_fp": 1, "das_ft": 2, "das_fpc": 3, "das_tjc": 4,
+              "das_runtime_w": 5, "das_tile": 6, "das_verbose": 7, "das_generic_tz": 8,
+              "fft_path": 9, "no_fused_display": 10, "fir_one_output": 11}
 
 
 class DasGeometry(ctypes.Structure):
@@ -49,9 +58,14 @@ SIGNATURES = {
     "bm_das_select": ([ctypes.POINTER(DasGeometry), _I64], ctypes.c_int),
     "bm_das_launch_shape": ([ctypes.POINTER(DasGeometry), _I64, _I32, _P], ctypes.c_int),
     "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
-    "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P], ctypes.c_int),
+    "bm_sigproc_ws_bytes": ([_I32, _I32, _I64, _I64, _I64], _I64),
+    "bm_pad_traces": ([_I32, _P, _I64, _I64, _I64, _P, _I64, _P], ctypes.c_int),
+    "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P, _I64, _P], ctypes.c_int),
     "bm_envelope": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
-    "bm_envelope_peak": ([_I32, _P, _P, _P, _I32, _I64, _I64, _P], ctypes.c_int),
+    "bm_abs": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
+    "bm_envelope_peak": ([_I32, _P, _P, _P, _I32, _I64, _I64, _P, _I64, _P], ctypes.c_int),
+    "bm_envelope_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _I64, _D, _P, _I64, _P],
+                            ctypes.c_int),
     "bm_fir_filter": ([_I32, _P, _I32, _P, _I64, _I64, _I64, _P, _I32, _P], ctypes.c_int),
     "bm_sliding_moments": ([_I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
                            ctypes.c_int),
@@ -59,9 +73,12 @@ SIGNATURES = {
     "bm_quantize_u8": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
     "bm_simulate_rf": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, _P, _I32,
                         _I32, _P, _P], ctypes.c_int),
+    "bm_display_tiles": ([_I32, _P, _I32, _I64, _I64, _I64, _P, _P, _D, _P], ctypes.c_int),
     "bm_frame_peak": ([_I32, _P, _P, _I32, _I64, _P], ctypes.c_int),
     "bm_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
     "bm_dynamic_adjustment": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
+    "bm_debug_set": ([_I32, _I32], ctypes.c_int),
+    "bm_debug_get": ([_I32], ctypes.c_int),
     "bm_error_string": ([ctypes.c_int], ctypes.c_char_p),
     "bm_abi_version": ([], ctypes.c_int),
 }
@@ -92,6 +109,36 @@ def check(code: int):
 
 def call(name: str, *args):
     check(getattr(load(), name)(*args))
+
+
+class debug_overrides:
+    """Context manager setting library test/tuning hooks (bm_debug_set), e.g.
+    ``with debug_overrides(das_fp=1, das_ft=2): ...``; restores the previous
+    values on exit.  The library reads no environment variables."""
+
+    def __init__(self, **kw):
+        self.kw = {DEBUG_KEYS[k]: int(v) for k, v in kw.items()}
+        self.prev = {}
+
+    def __enter__(self):
+        lib = load()
+        for k, v in self.kw.items():
+            self.prev[k] = lib.bm_debug_set(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        lib = load()
+        for k, v in self.prev.items():
+            lib.bm_debug_set(k, v)
+
+
+def workspace(nbytes: int, device):
+    """Caller-owned device workspace of at least ``nbytes`` (None if 0)."""
+    import torch
+
+    if nbytes <= 0:
+        return None
+    return torch.empty(int(nbytes), dtype=torch.uint8, device=device)
 
 
 def require_cuda():

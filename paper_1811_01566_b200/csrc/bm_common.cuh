@@ -5,6 +5,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "../../include/bmode200.h"
 
 namespace bm {
@@ -32,6 +34,12 @@ template <> struct R<double> {
   static __device__ __forceinline__ double from_double(double a) { return a; }
 };
 
+// bm_debug_set / bm_debug_get storage (one definition across translation units)
+inline std::atomic<int> g_debug_overrides[BM_DBG_COUNT];
+inline int debug_override(int key) {
+  return g_debug_overrides[key].load(std::memory_order_relaxed);
+}
+
 inline int cuda_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BM_OK : BM_ERR_CUDA;
@@ -48,33 +56,14 @@ inline int sm_count() {
   return n;
 }
 
-// fast (shared-memory-staged, f32x2) DAS paths: delay table in shared
-// memory (bm_das_fast.cu) or in tensor memory (bm_das_tmem.cu)
-int das_fast_eligible(const bm_das_geometry& g, int64_t rf_stride);
-int das_fast_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
-                    int64_t out_stride, int n_frames, cudaStream_t s);
-int das_tmem_eligible(const bm_das_geometry& g, int64_t rf_stride);
-int das_tmem_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
-                    int64_t out_stride, int n_frames, cudaStream_t s);
-int das_tmem_variant(const bm_das_geometry& g);
+// TMA DAS kernel (bm_das_tma.cu)
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);
 // returns -1 when this launch cannot use the TMA kernel (caller falls back)
 int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                    int64_t out_stride, int n_frames, cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid
 
-// DAS kernel selection: BM_DAS_KERNEL = auto (default) | tmem | smem | generic
-inline int das_kernel_choice() {
-  static int choice = -1;
-  if (choice < 0) {
-    const char* e = getenv("BM_DAS_KERNEL");
-    choice = 0;
-    if (e && !strcmp(e, "tmem")) choice = 1;
-    if (e && !strcmp(e, "smem")) choice = 2;
-    if (e && !strcmp(e, "generic")) choice = 3;
-    if (e && !strcmp(e, "tma")) choice = 4;
-  }
-  return choice;
-}
+// DAS kernel selection: 0 auto (TMA where it applies, else generic), 1 generic
+inline int das_kernel_choice() { return debug_override(BM_DBG_DAS_KERNEL); }
 
 }  // namespace bm

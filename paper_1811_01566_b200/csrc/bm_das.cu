@@ -203,8 +203,8 @@ static int launch_d(const DasArgs& a, int n_frames, cudaStream_t s) {
     const size_t cap = 227 * 1024;
     const size_t w1 = std::min<size_t>(cap / (per_px * kTileX + 1024), 32);
     const size_t w2 = 2 * std::min<size_t>(cap / (per_px * 2 * kTileX + 1024), 16);
-    const char* e = getenv("BM_DAS_GENERIC_TZ");  // A/B override: 1 | 2 | 4
-    const int tz = e ? atoi(e) : (w2 >= w1 ? 2 : 1);
+    const int otz = debug_override(BM_DBG_DAS_GENERIC_TZ);  // A/B override: 1 | 2 | 4
+    const int tz = otz ? otz : (w2 >= w1 ? 2 : 1);
     if (tz == 1) return launch_t<T, PW, LINEAR, UNIFORM, true, 1>(a, n_frames, s);
     if (tz == 2) return launch_t<T, PW, LINEAR, UNIFORM, true, 2>(a, n_frames, s);
   }
@@ -256,10 +256,7 @@ extern "C" int bm_das_aperture_span(const bm_das_geometry* g, double f_number,
 extern "C" int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride) {
   if (bm::check_geometry(g)) return -1;
   const int choice = bm::das_kernel_choice();
-  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride)) return 5;
-  if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
-    return 2 + bm::das_tmem_variant(*g);
-  if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride)) return 1;
+  if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride)) return 5;
   return 0;
 }
 
@@ -267,7 +264,7 @@ extern "C" int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_st
                                    int32_t n_frames, int32_t* shape) {
   if (!shape || bm::check_geometry(g)) return -1;
   const int choice = bm::das_kernel_choice();
-  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride))
+  if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride))
     return bm::das_tma_shape(*g, n_frames, shape);
   return -1;
 }
@@ -281,18 +278,38 @@ extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t
   if (n_frames == 0) return BM_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int choice = bm::das_kernel_choice();
-  if ((choice == 0 || choice == 4) && bm::das_tma_eligible(*g, rf_frame_stride)) {
+  if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride)) {
     rc = bm::das_tma_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
-    if (rc >= 0) return rc;  // -1: unaligned RF pointer etc. -> next kernel
+    if (rc >= 0) return rc;  // -1: unaligned RF pointer etc. -> generic kernel
   }
-  if ((choice == 0 || choice == 1) && bm::das_tmem_eligible(*g, rf_frame_stride))
-    return bm::das_tmem_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
-  if ((choice == 0 || choice == 2) && bm::das_fast_eligible(*g, rf_frame_stride))
-    return bm::das_fast_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
   bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride};
   if (g->dtype == BM_F32)
     return g->scheme == BM_PW ? bm::launch_p<float, true>(a, n_frames, s)
                               : bm::launch_p<float, false>(a, n_frames, s);
   return g->scheme == BM_PW ? bm::launch_p<double, true>(a, n_frames, s)
                             : bm::launch_p<double, false>(a, n_frames, s);
+}
+
+// Copy n_traces traces of n_samples samples (row pitch src_pitch) into rows of
+// dst_samples >= n_samples, zero-filling the tail: the TMA kernel's 16-B row
+// pitch for trace lengths that are not a multiple of 4 f32 samples.  The
+// padding reads as the zeros the reference's out-of-range sentinels stand
+// for (beamform.py:127-137), so the result is unchanged.  Two DMA operations,
+// no kernel.
+extern "C" int bm_pad_traces(int32_t dtype, const void* src, int64_t src_pitch, int64_t n_traces,
+                             int64_t n_samples, void* dst, int64_t dst_samples, void* stream) {
+  if (!src || !dst || n_traces < 0 || n_samples < 1 || dst_samples < n_samples ||
+      src_pitch < n_samples || (dtype != BM_F32 && dtype != BM_F64))
+    return BM_ERR_INVALID_ARGUMENT;
+  if (n_traces == 0) return BM_OK;
+  const size_t eb = dtype == BM_F64 ? 8 : 4;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpy2DAsync(dst, dst_samples * eb, src, src_pitch * eb, n_samples * eb, n_traces,
+                        cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return BM_ERR_CUDA;
+  if (dst_samples > n_samples &&
+      cudaMemset2DAsync((char*)dst + n_samples * eb, dst_samples * eb, 0,
+                        (dst_samples - n_samples) * eb, n_traces, s) != cudaSuccess)
+    return BM_ERR_CUDA;
+  return BM_OK;
 }

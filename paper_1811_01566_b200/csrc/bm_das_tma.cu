@@ -1,14 +1,13 @@
 // K1, warp-specialised: TMA-fed RF windows, receive delays in TENSOR MEMORY.
 //
-// Same arithmetic -- and therefore the same bits -- as das_tmem_kernel and
-// the reference's f32 das_beamform (beamform.py:122-187 with the DasPlan
-// delays of :211-228).  What changes is who moves the data:
+// Same arithmetic -- and therefore the same bits -- as the generic kernel
+// (bm_das.cu) and the reference's f32 das_beamform (beamform.py:122-187 with
+// the DasPlan delays of :211-228).  What changes is who moves the data (the
+// round-1 predecessor, where every warp issued its share of cp.async window
+// copies and met the others at one __syncthreads per chunk, spent ~35 % of its
+// warp samples outside the gather loop, profiles/r01_das_tmem_ncu.txt):
 //
-//  * das_tmem_kernel: every warp computes staging metadata, issues its share
-//    of the cp.async window copies and meets the others at one __syncthreads
-//    per chunk.  ncu (profiles/r01_das_tmem_ncu.txt) puts ~35 % of the warp
-//    samples of that kernel outside the gather/interpolate loop.
-//  * here a PRODUCER warp owns all of it: per stage of TJC receive channels
+//  * a PRODUCER warp owns all of it: per stage of TJC receive channels
 //    it computes each 4-channel group's window start, publishes the gather
 //    bases K, and issues one cp.async.bulk.tensor (TMA) box {W samples, 4
 //    traces, frames of the pass} per group (one trace per box for general
@@ -617,8 +616,7 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
   const int per_sm = 512 / tma_cols(g);
   const size_t cap = (size_t)(227 * 1024) / per_sm - 1024;
   const bool pw = g.scheme == BM_PW;
-  const char* ev = getenv("BM_DAS_TJC");  // tuning override: 32 | 64 | 128
-  const int only = ev ? atoi(ev) : 0;
+  const int only = debug_override(BM_DBG_DAS_TJC);  // tuning override: 32 | 64 | 128
   for (int t : {128, 64, 32, 16}) {
     if (t > g.n_rx && t > 32) continue;
     if (t == 128 && (!tma_has128(g) || fp != 1)) continue;
@@ -667,20 +665,18 @@ static bool tma_choose(const bm_das_geometry& g, int n_frames, TmaChoice& c) {
   while (fpc < 16 && fpc * 2 <= n_frames &&
          (int64_t)tiles * ((n_frames + fpc * 2 - 1) / (fpc * 2)) >= 4LL * per_sm * sm_count())
     fpc *= 2;
-  if (const char* e = getenv("BM_DAS_FPC")) {  // test hook: force the frames per CTA
-    const int want = atoi(e);
-    if (want >= 1) fpc = want < n_frames ? want : n_frames;
-  }
+  if (const int want = debug_override(BM_DBG_DAS_FPC); want >= 1)  // test hook
+    fpc = want < n_frames ? want : n_frames;
   c.fpc = fpc;
   // several frames per pass for identity-map apertures whenever a CTA owns
   // enough frames: fp consumer warp groups share one delay table (FP), each
   // thread accumulates ft frames (FT)
   c.fp = c.ft = 1;
   if (g.rx_contig) {
-    const char* e = getenv("BM_DAS_FP");   // tuning override: 1 | 2
-    const char* e2 = getenv("BM_DAS_FT");  // tuning override: 1 | 2 | 4 (the most tried)
-    const int want_fp = e && atoi(e) == 1 ? 1 : 2;
-    const int want_ft = e2 ? (atoi(e2) >= 4 ? 4 : atoi(e2) == 2 ? 2 : 1) : 4;
+    const int ofp = debug_override(BM_DBG_DAS_FP);  // tuning override: 1 | 2
+    const int oft = debug_override(BM_DBG_DAS_FT);  // tuning override: 1 | 2 | 4 (the most tried)
+    const int want_fp = ofp == 1 ? 1 : 2;
+    const int want_ft = oft ? (oft >= 4 ? 4 : oft == 2 ? 2 : 1) : 4;
     // several frames per thread: all-zero t0; non-uniform apodisation (its
     // w*(1-a), w*a shared by the frames too) with four frames per thread
     const bool ftn_ok = !g.t0_nonzero;
@@ -822,9 +818,9 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     // compile-time window widths for the uniform 16-channel kernels: the
     // frame-plane offsets of frames 1..3 become LDS immediates (cfg2: 12 %
     // fewer instructions in the gather loop, +3 % frames/s)
-    const char* ew = getenv("BM_DAS_WI");  // A/B override: 0 = runtime width
+    const bool rt_w = debug_override(BM_DBG_DAS_RUNTIME_W) > 0;  // A/B override
     const int wi = W == 96 ? 0 : W == 128 ? 1 : W == 160 ? 2 : W == 192 ? 3 : -1;
-    if (wi >= 0 && g.uniform && tjc == 16 && (!ew || atoi(ew) != 0)) {
+    if (wi >= 0 && g.uniform && tjc == 16 && !rt_w) {
 #define BM_TMA_WI(F, WV)                                                                   \
   das_tma_kernel<false, false, false, true, 16, false, F, 4, WV>,                          \
       das_tma_kernel<true, false, false, true, 16, false, F, 4, WV>,                       \
@@ -836,7 +832,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
 #undef BM_TMA_WI
       k = table7[(fp == 2 ? 16 : 0) + wi * 4 + (lin ? 2 : 0) + (pw ? 1 : 0)];
     }
-    if (W == 96 && !g.uniform && fp == 2 && (!ew || atoi(ew) != 0)) {
+    if (W == 96 && !g.uniform && fp == 2 && !rt_w) {
       // weighted (Hann / F-number), 96-sample windows: 16 / 32-channel stages
 #define BM_TMA_WIW(J)                                                                      \
   das_tma_kernel<false, false, false, true, J, true, 2, 4, 96>,                            \
@@ -852,8 +848,8 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
       cudaSuccess)
     return BM_ERR_CUDA;
   dim3 grid(tiles, (n_frames + fpc - 1) / fpc);
-  if (const char* e = getenv("BM_DAS_VERBOSE"))
-    if (atoi(e)) fprintf(stderr, "das_tma: fp=%d ft=%d tjc=%d nst=%d W=%d fpc=%d smem=%zu\n", fp, ft, tjc, nst, W, fpc, smem);
+  if (debug_override(BM_DBG_DAS_VERBOSE) > 0)
+    fprintf(stderr, "das_tma: fp=%d ft=%d tjc=%d nst=%d W=%d fpc=%d smem=%zu\n", fp, ft, tjc, nst, W, fpc, smem);
   k<<<grid, 32 * (4 * fp + 1), smem, s>>>(map, a);
   return cuda_status();
 }

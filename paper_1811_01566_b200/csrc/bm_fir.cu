@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kFirTile) fir_rows_kernel(const TI* __restrict
 template <typename TI, typename TO>
 static int fir_launch(const void* x, void* y, int64_t outer, int64_t n, int64_t inner,
                       const double* taps, int M, cudaStream_t s) {
-  if (inner == 1 && !getenv("BM_FIR_ONE_OUTPUT")) {  // test hook: force the one-output kernel
+  if (inner == 1 && debug_override(BM_DBG_FIR_ONE_OUTPUT) <= 0) {  // test hook: one-output kernel
     const int win = kFirR * kFirTile + M - 1;
     const size_t smem = (size_t)(M + fir_pad(win - 1) + 1) * sizeof(double);
     if (smem <= 200 * 1024) {

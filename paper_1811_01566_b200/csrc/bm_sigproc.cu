@@ -1,18 +1,36 @@
-// K2: analytic signal / envelope / dynamic adjustment (sm_100a).
+// K2/K3: analytic signal, envelope and dynamic adjustment (sm_100a).
 //
-// Replaces sigproc.py:48-97 (analytic_signal via scipy.fft, np.abs,
-// dynamic_adjustment).  For a power-of-two lane length the whole
-//   FFT -> one-sided gain -> IFFT -> |.| -> per-frame max
-// chain runs inside one CTA's shared memory (radix-2, L lanes per CTA), so
-// the complex I/Q data never touches HBM.  Other lengths use an exact
-// O(n^2) DFT per lane (same gain convention, sigproc.py:63-70).
-#include "bm_common.cuh"
+// Replaces sigproc.py:48-97: analytic_signal (scipy.fft), envelope (np.abs),
+// dynamic_adjustment (per-frame max, 20 log10, clip).  Lanes run along the
+// middle axis of an [outer][n][inner] array (axis 0 of an [n_z][n_x] image:
+// one lane per image column, pipeline.py:160).  Three execution paths, every
+// one O(n log n):
+//
+//   reg    f32, n = 256 / 512 / 1024 (every BASELINE config): one warp per
+//          lane, the lane's n samples in registers (analytic_reg_kernel).
+//   lane   any n whose prime factors are <= 61 and whose lanes fit in shared
+//          memory: mixed-radix DIF -> gain -> DIT in place in shared memory
+//          (analytic_lane_kernel, bm_fft.cuh).
+//   global everything else: the same stages as one launch each over a global
+//          buffer (smooth n), or Bluestein's chirp-z with power-of-two FFTs in
+//          f64 (n with a prime factor > 61).  Needs a caller workspace
+//          (bm_sigproc_ws_bytes).
+//
+// Fused display (bm_envelope_display, K2 + K3 in one launch): both on-chip
+// kernels run persistent.  A CTA keeps its columns' envelope in shared memory,
+// publishes the frame's running max (atomicMax on the IEEE bits) and a
+// per-frame completion count, and maps its columns to display values once
+// the count says every column of the frame is in -- so the envelope never
+// goes to HBM.  Items (frame, column block) are dealt round-robin to a
+// cooperative grid of G >= items-per-frame co-resident CTAs, and a CTA
+// computes its next item before it waits for the previous one's frame, so
+// every wait is on a frame whose items were all dealt out and are computed
+// without waiting (no deadlock).
+#include <algorithm>
+
+#include "bm_fft.cuh"
 
 namespace bm {
-
-template <typename T> struct C2;
-template <> struct C2<float> { using type = float2; };
-template <> struct C2<double> { using type = double2; };
 
 template <typename T> struct PeakBits;
 template <> struct PeakBits<float> {
@@ -26,21 +44,22 @@ template <> struct PeakBits<double> {
   static __device__ __forceinline__ double value(U b) { return __longlong_as_double((long long)b); }
 };
 
-// sigproc.py:63-70
+// max that lets NaN win (np.max propagates NaN; a NaN peak then fails the
+// reference's `peak > 0` test and raises AllZeroInput, sigproc.py:90-92).
+// Values are otherwise >= 0, so the IEEE bits order like the values, and a
+// NaN's bits (exponent all ones, mantissa != 0) sort above +inf.
 template <typename T>
-__device__ __forceinline__ T hilbert_gain(int64_t k, int64_t n) {
-  if (k == 0) return T(1);
-  if ((n & 1) == 0) {
-    if (k == n / 2) return T(1);
-    return k < n / 2 ? T(2) : T(0);
-  }
-  return k <= (n - 1) / 2 ? T(2) : T(0);
+__device__ __forceinline__ T nan_max(T v, T m) {
+  return (v != v || v > m) ? v : m;
 }
 
 template <typename T>
-__device__ __forceinline__ typename C2<T>::type cmul(typename C2<T>::type a,
-                                                     typename C2<T>::type b) {
-  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+__device__ __forceinline__ void block_peak(T v, typename PeakBits<T>::U* peak) {
+  for (int o = 16; o > 0; o >>= 1) v = nan_max(__shfl_xor_sync(0xffffffffu, v, o), v);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(peak, PeakBits<T>::bits(v));
+    __threadfence();
+  }
 }
 
 template <typename T>
@@ -49,261 +68,125 @@ __device__ __forceinline__ T magnitude(T re, T im) {
 }
 
 template <typename T>
-__device__ __forceinline__ void block_peak(T v, typename PeakBits<T>::U* peak) {
-  // warp max then one atomic per warp (values are >= 0, so IEEE bits order
-  // like the values)
-  for (int o = 16; o > 0; o >>= 1) {
-    T w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
-  }
-  if ((threadIdx.x & 31) == 0) atomicMax(peak, PeakBits<T>::bits(v));
-}
-
-enum OutMode { kComplex = 0, kEnvelope = 1 };
-
-// Power-of-two lanes: L (a power of two) lanes of length n per CTA, radix-2
-// DIT in shared memory.  All index arithmetic is 32-bit shifts and masks
-// (n, L powers of two); consecutive threads touch consecutive lanes on
-// global loads/stores (coalesced rows of L values) and consecutive
-// butterflies of one lane in shared memory.
-template <typename T, int MODE>
-__global__ void __launch_bounds__(256) analytic_pow2_kernel(const T* __restrict__ x, T* __restrict__ out,
-                                                            typename PeakBits<T>::U* __restrict__ peak,
-                                                            int n, int log2n, int64_t inner,
-                                                            int log2L) {
-  using V = typename C2<T>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int L = 1 << log2L;
-  V* tw = reinterpret_cast<V*>(smem_raw);  // [n/2]
-  V* buf = tw + n / 2;                       // [L][n]
-  const int64_t o = blockIdx.y;
-  const int64_t i_base = (int64_t)blockIdx.x * L;
-  const int half_n = n >> 1;
-  const int nt = blockDim.x;
-
-  for (int k = threadIdx.x; k < half_n; k += nt) {
-    double s, c;
-    sincospi(-2.0 * (double)k / (double)n, &s, &c);
-    tw[k] = V{(T)c, (T)s};
-  }
-  const T* xo = x + o * (int64_t)n * inner + i_base;
-  const bool full = i_base + L <= inner;
-  for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
-    const int l = idx & (L - 1), k = idx >> log2L;
-    const int r = __brev(k) >> (32 - log2n);
-    T v = T(0);
-    if (full || i_base + l < inner) v = xo[(int64_t)k * inner + l];
-    buf[(l << log2n) + r] = V{v, T(0)};
-  }
-  __syncthreads();
-
-  // FFT -> gain -> bit reversal -> inverse FFT, one warp per lane: the
-  // passes only need warp-level synchronisation
-  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31, nwarps = nt >> 5;
-  for (int l = warp; l < L; l += nwarps) {
-    V* lane = buf + (l << log2n);
-    for (int pass = 0; pass < 2; ++pass) {
-      const T sign = pass == 0 ? T(1) : T(-1);  // inverse: conjugate twiddles
-      for (int s = 1; s <= log2n; ++s) {
-        const int h = 1 << (s - 1);
-        for (int bb = wl; bb < half_n; bb += 32) {
-          const int pos = bb & (h - 1);
-          const int i = ((bb >> (s - 1)) << s) + pos;
-          V w = tw[pos << (log2n - s)];
-          w.y *= sign;
-          const V u = lane[i];
-          const V t = cmul<T>(w, lane[i + h]);
-          lane[i] = V{u.x + t.x, u.y + t.y};
-          lane[i + h] = V{u.x - t.x, u.y - t.y};
-        }
-        __syncwarp();
-      }
-      if (pass == 0) {
-        // one-sided gain, then bit-reverse permutation for the inverse DIT
-        for (int k = wl; k < n; k += 32) {
-          const int r = __brev(k) >> (32 - log2n);
-          if (k > r) continue;
-          const T gk = hilbert_gain<T>(k, n), gr = hilbert_gain<T>(r, n);
-          const V a = lane[k], bv = lane[r];
-          lane[k] = V{bv.x * gr, bv.y * gr};
-          lane[r] = V{a.x * gk, a.y * gk};
-        }
-        __syncwarp();
-      }
-    }
-  }
-  __syncthreads();
-
-  const T inv_n = T(1) / T(n);
-  T vmax = T(0);
-  for (int idx = threadIdx.x; idx < (n << log2L); idx += nt) {
-    const int l = idx & (L - 1), k = idx >> log2L;
-    if (!full && i_base + l >= inner) continue;
-    const V z = buf[(l << log2n) + k];
-    const T re = z.x * inv_n, im = z.y * inv_n;
-    const int64_t g = o * (int64_t)n * inner + (int64_t)k * inner + i_base + l;
-    if (MODE == kComplex) {
-      reinterpret_cast<V*>(out)[g] = V{re, im};
-    } else {
-      const T e = magnitude(re, im);
-      out[g] = e;
-      vmax = e > vmax ? e : vmax;
-    }
-  }
-  if (MODE == kEnvelope) block_peak<T>(vmax, peak + o);
-}
-
-// General n: exact DFT per lane (one lane per CTA).  Positive-frequency bins
-// only (the gain zeroes the rest), twiddles from an exact (j*k mod n) table.
-template <typename T, int MODE>
-__global__ void __launch_bounds__(256) analytic_dft_kernel(const T* __restrict__ x, T* __restrict__ out,
-                                                           typename PeakBits<T>::U* __restrict__ peak,
-                                                           int64_t n, int64_t inner) {
-  using V = typename C2<T>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* tw = reinterpret_cast<V*>(smem_raw);  // [n]
-  const int64_t nb = n / 2 + 1;           // bins 0..n/2
-  V* X = tw + n;                           // [nb]
-  T* xs = reinterpret_cast<T*>(X + nb);    // [n]
-  const int64_t o = blockIdx.y, i = blockIdx.x;
-  const int64_t base = o * n * inner + i;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-    double s, c;
-    sincospi(-2.0 * (double)k / (double)n, &s, &c);
-    tw[k] = V{(T)c, (T)s};
-    xs[k] = x[base + k * inner];
-  }
-  __syncthreads();
-  for (int64_t k = threadIdx.x; k < nb; k += blockDim.x) {
-    T re = 0, im = 0;
-    int64_t r = 0;
-    for (int64_t j = 0; j < n; ++j) {
-      const V w = tw[r];
-      re += xs[j] * w.x;
-      im += xs[j] * w.y;
-      r += k;
-      if (r >= n) r -= n;
-    }
-    const T g = hilbert_gain<T>(k, n);
-    X[k] = V{re * g, im * g};
-  }
-  __syncthreads();
-  const T inv_n = T(1) / T(n);
-  T vmax = T(0);
-  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
-    T re = 0, im = 0;
-    int64_t r = 0;
-    for (int64_t k = 0; k < nb; ++k) {
-      const V w = tw[r];  // exp(-2 pi i k t / n); inverse uses the conjugate
-      const V a = X[k];
-      re += a.x * w.x + a.y * w.y;
-      im += a.y * w.x - a.x * w.y;
-      r += t;
-      if (r >= n) r -= n;
-    }
-    re *= inv_n;
-    im *= inv_n;
-    if (MODE == kComplex) {
-      reinterpret_cast<V*>(out)[base + t * inner] = V{re, im};
-    } else {
-      const T e = magnitude(re, im);
-      out[base + t * inner] = e;
-      vmax = e > vmax ? e : vmax;
-    }
-  }
-  if (MODE == kEnvelope) block_peak<T>(vmax, peak + o);
-}
-
-template <typename T>
-__global__ void envelope_kernel(const T* __restrict__ z, T* __restrict__ e, int64_t count) {
-  using V = typename C2<T>::type;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const V v = reinterpret_cast<const V*>(z)[i];
-    e[i] = magnitude(v.x, v.y);
-  }
-}
-
-template <typename T>
-__global__ void peak_kernel(const T* __restrict__ e, typename PeakBits<T>::U* __restrict__ peak,
-                            int64_t frame_elems) {
-  const int64_t f = blockIdx.y;
-  const T* ef = e + f * frame_elems;
-  T vmax = T(0);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const T v = ef[i];
-    vmax = v > vmax ? v : vmax;
-  }
-  block_peak<T>(vmax, peak + f);
-}
-
-template <typename T>
-__device__ __forceinline__ T log10_rn(T v);
+__device__ __forceinline__ T log10_in(T v);
 template <>
-__device__ __forceinline__ float log10_rn<float>(float v) {
-  // f32 log10 (<= 2 ulp; exact 0 at the peak, where v == 1): the display
-  // tolerance vs numpy's own f32 log10 is 2e-6 of a [0, 1] display value
-  return log10f(v);
+__device__ __forceinline__ float log10_in<float>(float v) {
+  return log10f(v);  // <= 2 ulp; exactly 0 at the peak (v == 1)
 }
 template <>
-__device__ __forceinline__ double log10_rn<double>(double v) {
+__device__ __forceinline__ double log10_in<double>(double v) {
   return log10(v);
 }
 
-// sigproc.py:90-96, in the input precision: q = e/peak; db = 20*log10(q);
-// out = clip(db + R, 0, R) / R; zeros map to 0 without the log.
+// sigproc.py:93-96 in the input precision: q = e / peak, db = 20 log10 q,
+// clip(db + R, 0, R) / R; zeros (and anything the clip sends to 0 by a wide
+// margin, q < q0 = 0.999 * 10^(-R/20)) map to 0 without the log.
 template <typename T>
-__global__ void display_kernel(const T* __restrict__ e, const typename PeakBits<T>::U* __restrict__ peak,
-                               T* __restrict__ disp, int32_t* __restrict__ status,
-                               int64_t frame_elems, double range_db) {
+__device__ __forceinline__ T display_value(T v, T pk, T r, T q0) {
   using O = R<T>;
-  const int64_t f = blockIdx.y;
-  const T pk = PeakBits<T>::value(peak[f]);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && status) status[f] = pk > T(0) ? 0 : 1;
-  const T r = O::from_double(range_db);
-  // q = e/peak at least 0.1 % below 10^(-R/20) gives 20 log10 q + R < 0 with
-  // a margin far above every rounding of the chain: the clip makes it exactly
-  // 0, so the (f64) log is skipped -- most pixels of a 30 dB display
-  const T q0 = (T)(pow(10.0, -range_db / 20.0) * 0.999);
-  const T* ef = e + f * frame_elems;
-  T* df = disp + f * frame_elems;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const T v = ef[i];
-    T outv = T(0);
-    const T q = O::div(v, pk);
-    if (v > T(0) && pk > T(0) && !(q < q0)) {
-      const T db = O::mul(T(20), log10_rn<T>(q));
-      T s = O::add(db, r);
-      s = s < T(0) ? T(0) : (s > r ? r : s);
-      outv = O::div(s, r);
-    }
-    df[i] = outv;
+  if (!(v > T(0)) || !(pk > T(0))) return T(0);
+  const T q = O::div(v, pk);
+  if (q < q0) return T(0);
+  const T db = O::mul(T(20), log10_in<T>(q));
+  T s = O::add(db, r);
+  s = s < T(0) ? T(0) : (s > r ? r : s);
+  return O::div(s, r);
+}
+
+// Same mapping, with the early-out tested as v < cut = q0 * peak (no
+// division): q0 sits 0.1 % below the clip threshold, far beyond the one
+// rounding of the product, so every pixel it sends to 0 maps to 0 exactly.
+template <typename T>
+__device__ __forceinline__ T display_value_cut(T v, T pk, T r, T cut) {
+  using O = R<T>;
+  if (!(v > T(0)) || !(pk > T(0)) || v < cut) return T(0);
+  const T db = O::mul(T(20), log10_in<T>(O::div(v, pk)));
+  T s = O::add(db, r);
+  s = s < T(0) ? T(0) : (s > r ? r : s);
+  return O::div(s, r);
+}
+
+enum OutMode { kComplex = 0, kEnvelope = 1, kDisplay = 2 };
+
+// ---- fused-display frame synchronisation -------------------------------------
+__device__ __forceinline__ void frame_wait(const int* done, int target) {
+  int v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (v >= target) return;
+    __nanosleep(64);
   }
 }
 
-static inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
-static inline int ilog2(int64_t n) {
-  int l = 0;
-  while (((int64_t)1 << l) < n) ++l;
-  return l;
+// Called by all threads after the CTA's block_peak of a frame's item:
+// publishes one finished item of frame o.
+__device__ __forceinline__ void frame_signal(int* done) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(done, 1);
+  }
 }
 
+// Waits until frame o is complete and returns its peak (all threads).
+template <typename T>
+__device__ __forceinline__ T frame_peak(const int* done, int per_frame,
+                                        const typename PeakBits<T>::U* peak, T* bcast) {
+  if (threadIdx.x == 0) {
+    frame_wait(done, per_frame);
+    *bcast = PeakBits<T>::value(__ldcg(peak));
+  }
+  __syncthreads();
+  return *bcast;
+}
+
+struct DispArgs {
+  int32_t* status;
+  int* done;       // [n_frames] completed items per frame (zeroed by the launcher)
+  double range_db;
+};
+
+template <typename T>
+struct DispConst {
+  T r, q0;
+  __device__ DispConst(double range_db)
+      : r(R<T>::from_double(range_db)), q0((T)(pow(10.0, -range_db / 20.0) * 0.999)) {}
+};
 
 // ---------------------------------------------------------------------------
-// f32 lanes of n = 32 * R samples (R = 8, 16, 32: n = 256 .. 1024), one WARP
-// per lane, data in REGISTERS.  With j = t + 32 i (t = lane, i < R) and
-// k = k1 + R k2:
-//   X[k1 + R k2] = sum_t W32^(t k2) * [ Wn^(t k1) * sum_i x[t + 32 i] WR^(i k1) ]
-// so a lane's transform is an R-point DFT inside each thread (radix-2 DIF,
+// Two real lanes per complex transform.  With g = 1 + s, s = sgn(k) (0 at DC
+// and Nyquist; sigproc.py:63-70), the analytic signal of a real lane is
+//   z = ifft(g fft(x)) = x + i h,   h = ifft(-i s fft(x))   (real),
+// and since the transform is linear with a real kernel, one complex FFT pair
+// gives the Hilbert transforms of two lanes at once:
+//   h_a + i h_b = ifft(-i s fft(x_a + i x_b)).
+// So every path computes z = (x, h): the real part is the input itself (the
+// reference's real part is x up to FFT round-off, sigproc.py:51-55) and
+// |z| = hypot(x, h).  Half the transforms of one complex FFT pair per lane.
+template <typename V>
+__device__ __forceinline__ V hilbert_rot(V v, int s) {  // -i s v
+  using T = decltype(v.x);
+  return s > 0 ? V{v.y, -v.x} : (s < 0 ? V{-v.y, v.x} : V{T(0), T(0)});
+}
+
+__device__ __forceinline__ int hilbert_sign(int64_t k, int64_t n) {
+  if (k == 0 || 2 * k == n) return 0;
+  return 2 * k < n ? 1 : -1;
+}
+
+// ---------------------------------------------------------------------------
+// reg: f32 lanes of n = 32 R samples (R = 8, 16, 32), one WARP per PAIR of
+// lanes, the packed pair in REGISTERS.  With j = t + 32 i (t = lane, i < R)
+// and k = k1 + R k2:
+//   X[k1 + R k2] = sum_t W32^(t k2) * [ Wn^(t k1) * sum_i w[t + 32 i] WR^(i k1) ]
+// so the transform is an R-point DFT inside each thread (radix-2 DIF,
 // compile-time register indices), a per-thread twiddle, and a 32-point DFT
 // across the warp (radix-2 DIF over __shfl_xor).  The spectrum ends up
-// bit-reversed in both indices, which the one-sided gain reads directly; the
-// inverse runs the mirror image (DIT across lanes, twiddle, DIT in registers)
-// and lands in natural order.  Shared memory holds only the twiddle table and
-// the CTA's [n][8] tile for coalesced 32-B row loads and stores: two
-// __syncthreads per CTA instead of one __syncwarp per radix-2 pass.
+// bit-reversed in both indices, which the Hilbert rotation reads directly;
+// the inverse runs the mirror image (DIT across lanes, twiddle, DIT in
+// registers) and lands in natural order.  A CTA (8 warps) owns 16 adjacent
+// columns: the [n][17] shared tile gives coalesced 64-B row loads/stores and
+// conflict-free column reads.
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return {a.x + b.x, a.y + b.y}; }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return {a.x - b.x, a.y - b.y}; }
 __device__ __forceinline__ float2 c_mul(float2 a, float2 w) {
@@ -319,45 +202,10 @@ __device__ __forceinline__ int brev_c(int p) {  // bit reversal of p in log2(R) 
   return r;
 }
 
-template <int MODE, int R>
-__global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restrict__ x,
-                                                           float* __restrict__ out,
-                                                           unsigned* __restrict__ peak,
-                                                           int64_t inner) {
-  constexpr int N = 32 * R, L = 8, LP = L + 1;  // LP: padded tile row (conflict-free columns)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* tw = reinterpret_cast<float2*>(smem_raw);  // [N] Wn^m
-  float* tile = reinterpret_cast<float*>(tw + N);     // real: [N][LP]; complex: [N][LP] float2
-  const int tid = threadIdx.x, warp = tid >> 5, t = tid & 31;
-  const int64_t o = blockIdx.y, i_base = (int64_t)blockIdx.x * L;
-  const int lanes = (int)(inner - i_base < L ? inner - i_base : L);
-
-  for (int m = tid; m < N; m += 256) {
-    double sn, cs;
-    sincospi(-2.0 * (double)m / (double)N, &sn, &cs);
-    tw[m] = make_float2((float)cs, (float)sn);
-  }
-  const float* xo = x + o * (int64_t)N * inner + i_base;
-  {
-    // all R loads of a thread in flight before the first shared-memory store
-    float ld[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int idx = tid + 256 * q, l = idx & (L - 1), k = idx >> 3;
-      ld[q] = l < lanes ? __ldg(xo + (int64_t)k * inner + l) : 0.0f;
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int idx = tid + 256 * q;
-      tile[(idx >> 3) * LP + (idx & (L - 1))] = ld[q];
-    }
-  }
-  __syncthreads();
-
-  float2 v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = make_float2(tile[(t + 32 * i) * LP + warp], 0.0f);
-
+// v[i] = w[t + 32 i] in, v[i] = N * ifft(-i s fft(w))[t + 32 i] out.
+template <int R>
+__device__ __forceinline__ void reg_pair_hilbert(const float2* tw, int t, float2 (&v)[R]) {
+  constexpr int N = 32 * R;
   // (1) R-point DFT over i in registers, radix-2 DIF: v[p] = A[brev(p)]
 #pragma unroll
   for (int h = R / 2; h >= 1; h >>= 1)
@@ -385,15 +233,11 @@ __global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restri
       v[p] = up ? c_mul(c_sub(q, v[p]), w) : c_add(v[p], q);
     }
   }
-  // (4) one-sided gain (sigproc.py:63-70) at k = k1 + R k2
+  // (4) Hilbert rotation -i sgn(k) at k = k1 + R k2
   {
     const int k2 = __brev(t) >> 27;
 #pragma unroll
-    for (int p = 0; p < R; ++p) {
-      const int k = brev_c<R>(p) + R * k2;
-      const float gk = (k == 0 || k == N / 2) ? 1.0f : (k < N / 2 ? 2.0f : 0.0f);
-      v[p] = make_float2(v[p].x * gk, v[p].y * gk);
-    }
+    for (int p = 0; p < R; ++p) v[p] = hilbert_rot(v[p], hilbert_sign(brev_c<R>(p) + R * k2, N));
   }
   // (5) inverse 32-point DIT across the warp (bit-reversed in, natural out)
 #pragma unroll
@@ -412,7 +256,7 @@ __global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restri
   // (6) twiddle Wn^(-t k1)
 #pragma unroll
   for (int p = 1; p < R; ++p) v[p] = c_mul(v[p], c_conj(tw[t * brev_c<R>(p)]));
-  // (7) inverse R-point DIT in registers: v[i] = n * x'[t + 32 i]
+  // (7) inverse R-point DIT in registers
 #pragma unroll
   for (int h = 1; h < R; h <<= 1)
 #pragma unroll
@@ -424,114 +268,711 @@ __global__ void __launch_bounds__(256) analytic_reg_kernel(const float* __restri
         v[b + j] = c_add(a, c);
         v[b + j + h] = c_sub(a, c);
       }
+}
 
-  __syncthreads();  // tile reused for the output
-  const float inv_n = 1.0f / (float)N;
-  float vmax = 0.0f;
-  if (MODE == kComplex) {
-    float2* tc = reinterpret_cast<float2*>(tile);
+template <int MODE, int R>
+struct RegCfg {
+  static constexpr int N = 32 * R, L = 16, LP = 17;
+  static constexpr int NB = MODE == kDisplay ? 2 : 1;  // tiles (double buffer)
+  static constexpr int TILE = N * LP;                  // floats per tile
+  static constexpr size_t smem = (size_t)N * 8 + (size_t)NB * TILE * 4 + 16;
+  static constexpr int MINB = R == 8 ? 3 : (R == 16 ? 2 : 1);
+};
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(256, (RegCfg<MODE, R>::MINB))
+    analytic_reg_kernel(const float* __restrict__ x, float* __restrict__ out,
+                        unsigned* __restrict__ peak, int64_t n_items, int64_t per_frame,
+                        int64_t inner, DispArgs da) {
+  using C = RegCfg<MODE, R>;
+  constexpr int N = C::N, L = C::L, LP = C::LP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);  // [N] Wn^m
+  float* tiles = reinterpret_cast<float*>(tw + N);
+  float* bcast = tiles + C::NB * C::TILE;
+  const int tid = threadIdx.x, warp = tid >> 5, t = tid & 31;
+  const DispConst<float> dc(da.range_db);
+
+  for (int m = tid; m < N; m += 256) {
+    double sn, cs;
+    sincospi(-2.0 * (double)m / (double)N, &sn, &cs);
+    tw[m] = make_float2((float)cs, (float)sn);
+  }
+
+  // display of one finished item (its envelope in `tile`): waits for the frame
+  auto map_item = [&](int64_t item, const float* tile) {
+    const int64_t o = item / per_frame, blk = item - o * per_frame, i_base = blk * L;
+    const int lanes = (int)(inner - i_base < L ? inner - i_base : L);
+    const float pk = frame_peak<float>(da.done + o, (int)per_frame, peak + o, bcast);
+    if (blk == 0 && tid == 0 && da.status) da.status[o] = pk > 0.0f ? 0 : 1;
+    const float cut = dc.q0 * pk;
+    float* dst = out + o * (int64_t)N * inner + i_base;
+    for (int idx = tid; idx < N * L; idx += 256) {
+      const int l = idx & (L - 1), k = idx >> 4;
+      if (l < lanes) dst[(int64_t)k * inner + l] =
+          display_value_cut<float>(tile[k * LP + l], pk, dc.r, cut);
+    }
+    __syncthreads();  // tile free again
+  };
+
+  int64_t prev = -1;
+  int j = 0;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
+    float* tile = tiles + (j % C::NB) * C::TILE;
+    const int64_t o = item / per_frame, i_base = (item - o * per_frame) * L;
+    const int lanes = (int)(inner - i_base < L ? inner - i_base : L);
+    const float* xo = x + o * (int64_t)N * inner + i_base;
+    // 2R loads per thread, issued in groups of 16 before their shared-memory
+    // stores (enough in flight to cover the latency, few registers)
 #pragma unroll
-    for (int i = 0; i < R; ++i)
-      tc[(t + 32 * i) * LP + warp] = make_float2(v[i].x * inv_n, v[i].y * inv_n);
-  } else {
+    for (int q0 = 0; q0 < 2 * R; q0 += 16) {
+      float ld[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int idx = tid + 256 * (q0 + q), l = idx & (L - 1), k = idx >> 4;
+        ld[q] = l < lanes ? __ldg(xo + (int64_t)k * inner + l) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int idx = tid + 256 * (q0 + q);
+        tile[(idx >> 4) * LP + (idx & (L - 1))] = ld[q];
+      }
+    }
+    __syncthreads();  // also orders the twiddle table before its first use
+
+    // warp w packs columns 2w (real) and 2w + 1 (imaginary)
+    const int ca = 2 * warp, cb = ca + 1;
+    float2 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const float e = magnitude(v[i].x * inv_n, v[i].y * inv_n);
-      tile[(t + 32 * i) * LP + warp] = e;
-      if (warp < lanes) vmax = e > vmax ? e : vmax;
+      const int r = (t + 32 * i) * LP;
+      v[i] = make_float2(tile[r + ca], tile[r + cb]);
+    }
+    reg_pair_hilbert<R>(tw, t, v);
+    const float inv_n = 1.0f / (float)N;
+    float vmax = 0.0f;
+    // each warp rewrites only its own two columns: the Hilbert transform for
+    // complex output, the envelope hypot(x, h) otherwise
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = (t + 32 * i) * LP;
+      const float ha = v[i].x * inv_n, hb = v[i].y * inv_n;
+      if (MODE == kComplex) {
+        tile[r + ca] = ha;
+        tile[r + cb] = hb;
+      } else {
+        const float ea = magnitude(tile[r + ca], ha), eb = magnitude(tile[r + cb], hb);
+        tile[r + ca] = ea;
+        tile[r + cb] = eb;
+        if (ca < lanes) vmax = nan_max(ea, vmax);
+        if (cb < lanes) vmax = nan_max(eb, vmax);
+      }
+    }
+    if (MODE == kDisplay) {
+      block_peak<float>(vmax, peak + o);
+      frame_signal(da.done + o);  // includes the barrier that completes the tile
+      if (prev >= 0) map_item(prev, tiles + ((j + 1) % C::NB) * C::TILE);
+      prev = item;
+      continue;
+    }
+    __syncthreads();
+    const int64_t g0 = o * (int64_t)N * inner + i_base;
+    for (int idx = tid; idx < N * L; idx += 256) {
+      const int l = idx & (L - 1), k = idx >> 4;
+      if (l >= lanes) continue;
+      const int64_t g = g0 + (int64_t)k * inner + l;
+      if (MODE == kComplex)
+        reinterpret_cast<float2*>(out)[g] = make_float2(__ldg(x + g), tile[k * LP + l]);
+      else
+        out[g] = tile[k * LP + l];
+    }
+    if (MODE == kEnvelope) block_peak<float>(vmax, peak + o);
+    __syncthreads();  // tile reused by the next item
+  }
+  if (MODE == kDisplay && prev >= 0) map_item(prev, tiles + ((j + 1) % C::NB) * C::TILE);
+}
+
+// ---------------------------------------------------------------------------
+// lane: L lanes (a power of two <= 16) per item in shared memory, packed in
+// pairs (x_a + i x_b) into max(1, L/2) complex buffers; mixed radix.
+__host__ __device__ __forceinline__ int lane_bufs(int L) { return L > 1 ? L / 2 : 1; }
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+    analytic_lane_kernel(const T* __restrict__ x, T* __restrict__ out,
+                         typename PeakBits<T>::U* __restrict__ peak, FftPlan p, int64_t n_items,
+                         int64_t per_frame, int64_t inner, int L, int lstride, DispArgs da) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = p.n, nlo = 1 << p.tw_shift, nhi = (n + nlo - 1) >> p.tw_shift;
+  V* lo = reinterpret_cast<V*>(smem_raw);
+  V* hi = lo + nlo;
+  V* buf = hi + nhi;
+  T* bcast = reinterpret_cast<T*>(buf + (size_t)lane_bufs(L) * lstride);
+  T* comp = reinterpret_cast<T*>(buf);  // lane l at comp[2 (l/2) lstride + 2 k + (l & 1)]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const Twiddle<T> tw{hi, lo, p.tw_shift, nlo - 1};
+  twiddle_tables<T>(hi, lo, n, p.tw_shift, tid, nthr);
+  const DispConst<T> dc(da.range_db);
+  const int log2L = __ffs(L) - 1;
+  const T inv_n = T(1) / T(n);
+  auto at = [&](int l, int k) { return 2 * (l >> 1) * lstride + 2 * k + (l & 1); };
+
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int64_t o = item / per_frame, blk = item - o * per_frame, i_base = blk * L;
+    const int nl = (int)(inner - i_base < L ? inner - i_base : L);
+    const int nb = (nl + 1) / 2;  // packed buffers in use
+    const int64_t g0 = o * (int64_t)n * inner + i_base;
+    for (int idx = tid; idx < (n << log2L); idx += nthr) {
+      const int l = idx & (L - 1), k = idx >> log2L;
+      comp[at(l, k)] = l < nl ? x[g0 + (int64_t)k * inner + l] : T(0);
+    }
+    if (L == 1)
+      for (int k = tid; k < n; k += nthr) comp[2 * k + 1] = T(0);
+    __syncthreads();
+    lane_dif<T>(buf, lstride, nb, p, tw, tid, nthr);
+    for (int pos = tid; pos < n; pos += nthr) {
+      const int sg = hilbert_sign(unscramble(p, pos), n);
+      for (int b = 0; b < nb; ++b) buf[b * lstride + pos] = hilbert_rot(buf[b * lstride + pos], sg);
+    }
+    __syncthreads();
+    lane_dit<T>(buf, lstride, nb, p, tw, tid, nthr);
+    T vmax = T(0);
+    for (int idx = tid; idx < (n << log2L); idx += nthr) {
+      const int l = idx & (L - 1), k = idx >> log2L;
+      if (l >= nl) continue;
+      const int64_t g = g0 + (int64_t)k * inner + l;
+      const T h = comp[at(l, k)] * inv_n, xv = x[g];
+      if (MODE == kComplex) {
+        reinterpret_cast<V*>(out)[g] = V{xv, h};
+      } else {
+        const T e = magnitude(xv, h);
+        vmax = nan_max(e, vmax);
+        if (MODE == kEnvelope) out[g] = e;
+        else comp[at(l, k)] = e;  // own element: no hazard
+      }
+    }
+    if (MODE != kComplex) block_peak<T>(vmax, peak + o);
+    if (MODE == kDisplay) {
+      frame_signal(da.done + o);
+      const T pk = frame_peak<T>(da.done + o, (int)per_frame, peak + o, bcast);
+      if (blk == 0 && tid == 0 && da.status) da.status[o] = pk > T(0) ? 0 : 1;
+      const T cut = dc.q0 * pk;
+      for (int idx = tid; idx < (n << log2L); idx += nthr) {
+        const int l = idx & (L - 1), k = idx >> log2L;
+        if (l < nl)
+          out[g0 + (int64_t)k * inner + l] = display_value_cut<T>(comp[at(l, k)], pk, dc.r, cut);
+      }
+    }
+    __syncthreads();  // buffer reused by the next item
+  }
+}
+
+// ---------------------------------------------------------------------------
+// global: one launch per stage over [outer][n][inner] complex buffers
+// (element (lane, pos) at ((o n) + pos) inner + i, lane = o inner + i; a
+// Bluestein work buffer is the case outer = 1).  Threads run lane-fastest, so
+// every access is coalesced across lanes.
+struct GLay {
+  int64_t outer, n, inner;
+  __device__ __forceinline__ int64_t at(int64_t lane, int64_t pos) const {
+    const int64_t o = lane / inner, i = lane - o * inner;
+    return (o * n + pos) * inner + i;
+  }
+  __device__ __forceinline__ int64_t lanes() const { return outer * inner; }
+};
+
+template <typename T, int R, bool DIT>
+__global__ void g_stage_kernel(typename C2<T>::type* buf, GLay lay, int span, int radix) {
+  const int n = (int)lay.n;
+  const int Rr = R ? R : radix;
+  const int64_t lanes = lay.lanes(), nb = n / Rr, total = nb * lanes;
+  const TwiddleDirect<T> tw{n};
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lane = idx % lanes;
+    const int b = (int)(idx / lanes);
+    if (!DIT) {
+      const int sub = span / Rr, g = b / sub, k = b - g * sub;
+      auto* base = buf + lay.at(lane, (int64_t)g * span + k);
+      const int64_t stride = (int64_t)sub * lay.inner;
+      const int e1 = k * (n / span);
+      if constexpr (R != 0) dif_bfly<R, T>(base, stride, e1, tw);
+      else generic_bfly<-1, T>(base, stride, Rr, n, e1, tw);
+    } else {
+      const int ns = span * Rr, g = b / span, k = b - g * span;
+      auto* base = buf + lay.at(lane, (int64_t)g * ns + k);
+      const int64_t stride = (int64_t)span * lay.inner;
+      const int e1 = k * (n / ns);
+      if constexpr (R != 0) dit_bfly<R, T>(base, stride, e1, tw);
+      else generic_bfly<+1, T>(base, stride, Rr, n, e1, tw);
     }
   }
-  __syncthreads();
-  const int64_t g0 = o * (int64_t)N * inner + i_base;
-  for (int idx = tid; idx < N * L; idx += 256) {
-    const int l = idx & (L - 1), k = idx >> 3;
-    if (l >= lanes) continue;
-    if (MODE == kComplex)
-      reinterpret_cast<float2*>(out)[g0 + (int64_t)k * inner + l] =
-          reinterpret_cast<const float2*>(tile)[k * LP + l];
-    else
-      out[g0 + (int64_t)k * inner + l] = tile[k * LP + l];
+}
+
+static inline unsigned g_blocks(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  const int64_t cap = 16LL * sm_count();
+  return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+template <typename T>
+static int g_fft(typename C2<T>::type* buf, const GLay& lay, const FftPlan& p, bool inverse,
+                 cudaStream_t s) {
+  const int64_t lanes = lay.outer * lay.inner;
+  if (!inverse) {
+    int span = p.n;
+    for (int i = 0; i < p.m; ++i) {
+      const int r = p.radix[i];
+      const unsigned gb = g_blocks(lanes * (p.n / r));
+      if (r == 8) g_stage_kernel<T, 8, false><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else if (r == 4) g_stage_kernel<T, 4, false><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else if (r == 2) g_stage_kernel<T, 2, false><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else g_stage_kernel<T, 0, false><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      span /= r;
+    }
+  } else {
+    int span = 1;
+    for (int i = p.m - 1; i >= 0; --i) {
+      const int r = p.radix[i];
+      const unsigned gb = g_blocks(lanes * (p.n / r));
+      if (r == 8) g_stage_kernel<T, 8, true><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else if (r == 4) g_stage_kernel<T, 4, true><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else if (r == 2) g_stage_kernel<T, 2, true><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      else g_stage_kernel<T, 0, true><<<gb, 256, 0, s>>>(buf, lay, span, r);
+      span *= r;
+    }
   }
-  if (MODE == kEnvelope) block_peak<float>(vmax, peak + o);
+  return cuda_status();
+}
+
+template <typename T>
+__global__ void g_load_kernel(const T* __restrict__ x, typename C2<T>::type* buf, GLay lay) {
+  const int64_t total = lay.lanes() * lay.n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = {x[i], T(0)};  // same [outer][n][inner] layout
+}
+
+template <typename T>
+__global__ void g_gain_kernel(typename C2<T>::type* buf, GLay lay, FftPlan p) {
+  const int64_t lanes = lay.lanes(), total = lanes * lay.n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lane = idx % lanes;
+    const int pos = (int)(idx / lanes);
+    const T g = hilbert_gain<T>(unscramble(p, pos), lay.n);
+    auto& e = buf[lay.at(lane, pos)];
+    e = {e.x * g, e.y * g};
+  }
+}
+
+// Final scale (x 1/n) into z (complex) or |z| into env with per-frame peaks.
+template <typename T, int MODE>
+__global__ void g_out_kernel(typename C2<T>::type* buf, T* __restrict__ out,
+                             typename PeakBits<T>::U* __restrict__ peak, GLay lay, T scale) {
+  const int64_t per = lay.n * lay.inner;
+  for (int64_t o = blockIdx.y; o < lay.outer; o += gridDim.y) {
+    T vmax = T(0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const auto z = buf[o * per + i];
+      const T re = z.x * scale, im = z.y * scale;
+      if (MODE == kComplex) {
+        reinterpret_cast<typename C2<T>::type*>(out)[o * per + i] = {re, im};
+      } else {
+        const T e = magnitude(re, im);
+        out[o * per + i] = e;
+        vmax = nan_max(e, vmax);
+      }
+    }
+    if (MODE != kComplex) block_peak<T>(vmax, peak + o);
+  }
+}
+
+// ---- Bluestein (chirp-z), f64, for lengths with a prime factor > 61 ---------
+// X_k = c_k sum_m (x_m c_m) conj(c_(k-m)),  c_m = exp(-i pi m^2 / n): a
+// cyclic convolution of length M (a power of two >= 2n - 1) done with the
+// power-of-two FFT stages; the inverse n-point DFT uses conj(DFT(conj X)) / n.
+__global__ void bs_chirp_kernel(double2* c, int64_t n) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = ((uint64_t)m * (uint64_t)m) % (uint64_t)(2 * n);  // exact
+    double s, co;
+    sincospi(-(double)e / (double)n, &s, &co);
+    c[m] = {co, s};
+  }
+}
+
+__global__ void bs_bprep_kernel(double2* b, const double2* __restrict__ c, int64_t n, int64_t M) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = {0.0, 0.0};
+    if (m < n) v = cconj(c[m]);
+    else if (m > M - n) v = cconj(c[M - m]);
+    b[m] = v;
+  }
+}
+
+// work[m][lc] = x(lane c0 + lc)[m] c_m  (zero for m >= n)
+template <typename T>
+__global__ void bs_load_kernel(double2* work, const T* __restrict__ x, const double2* __restrict__ c,
+                               GLay xl, int64_t c0, int64_t lc_n, int64_t M) {
+  const int64_t total = lc_n * M;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lc = idx % lc_n, m = idx / lc_n;
+    double2 v = {0.0, 0.0};
+    if (m < xl.n) {
+      const double xv = (double)x[xl.at(c0 + lc, m)];
+      v = {xv * c[m].x, xv * c[m].y};
+    }
+    work[idx] = v;
+  }
+}
+
+__global__ void bs_mulb_kernel(double2* work, const double2* __restrict__ bh, int64_t lc_n,
+                               int64_t M) {
+  const int64_t total = lc_n * M;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    work[idx] = cmul(work[idx], bh[idx / lc_n]);
+}
+
+// X_k = c_k conv_k / M, times the gain; then the next input conj(X_k) c_k.
+__global__ void bs_mid_kernel(double2* work, const double2* __restrict__ c, int64_t n,
+                              int64_t lc_n, int64_t M) {
+  const int64_t total = lc_n * M;
+  const double inv_m = 1.0 / (double)M;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx / lc_n;
+    double2 v = {0.0, 0.0};
+    if (k < n) {
+      const double2 w = work[idx];
+      const double g = hilbert_gain<double>(k, n) * inv_m;
+      const double2 X = cmul(c[k], double2{w.x * g, w.y * g});
+      v = cmul(cconj(X), c[k]);
+    }
+    work[idx] = v;
+  }
 }
 
 template <typename T, int MODE>
-static int launch_analytic_reg(const T*, T*, typename PeakBits<T>::U*, int64_t, int64_t, int64_t,
-                               cudaStream_t) {
-  return -1;  // f64: shared-memory radix-2 kernel
+__global__ void bs_out_kernel(const double2* __restrict__ work, const double2* __restrict__ c,
+                              T* __restrict__ out, typename PeakBits<T>::U* __restrict__ peak,
+                              GLay xl, int64_t c0, int64_t lc_n, int64_t M) {
+  const int64_t total = lc_n * xl.n;
+  const double sc = 1.0 / ((double)M * (double)xl.n);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lc = idx % lc_n, m = idx / lc_n, lane = c0 + lc;
+    const double2 y = cmul(c[m], work[m * lc_n + lc]);
+    const T re = (T)(y.x * sc), im = (T)(-y.y * sc);
+    const int64_t at = xl.at(lane, m);
+    if (MODE == kComplex) {
+      reinterpret_cast<typename C2<T>::type*>(out)[at] = {re, im};
+    } else {
+      const T e = magnitude(re, im);
+      out[at] = e;
+      if (e != T(0) || e != e) atomicMax(peak + lane / xl.inner, PeakBits<T>::bits(nan_max(e, T(0))));
+    }
+  }
 }
-template <>
-int launch_analytic_reg<float, kEnvelope>(const float*, float*, unsigned*, int64_t, int64_t,
-                                          int64_t, cudaStream_t);
-template <>
-int launch_analytic_reg<float, kComplex>(const float*, float*, unsigned*, int64_t, int64_t,
-                                         int64_t, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// host-side path choice
+enum { kPathReg = 0, kPathLane = 1, kPathGlobal = 2, kPathBluestein = 3 };
+constexpr size_t kLaneSmemMulti = 100 * 1024;   // L > 1: keep >= 2 CTAs per SM
+constexpr size_t kLaneSmemMax = 200 * 1024;
+constexpr int64_t kBluesteinWorkBytes = 64LL << 20;
+
+struct SigPlan {
+  int path;
+  FftPlan p;
+  int L, lstride;
+  size_t smem;
+  int64_t M, LC;  // Bluestein
+  FftPlan pm;
+};
+
+static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+template <typename T>
+static size_t lane_smem(const FftPlan& p, int L, int lstride) {
+  const int nlo = 1 << p.tw_shift, nhi = (p.n + nlo - 1) >> p.tw_shift;
+  return (size_t)(nlo + nhi + (size_t)lane_bufs(L) * lstride) * sizeof(typename C2<T>::type) + 16;
+}
+
+static int sig_plan(int32_t dtype, int64_t n, int64_t outer, int64_t inner, SigPlan* sp) {
+  if (n > 0x7fffffffLL / 2 || outer < 1 || inner < 1) return BM_ERR_UNSUPPORTED;
+  *sp = SigPlan{};
+  sp->p = make_plan(n);
+  if (dtype == BM_F32 && (n == 256 || n == 512 || n == 1024) && debug_override(BM_DBG_FFT_PATH) <= 0) {
+    sp->path = kPathReg;
+    return BM_OK;
+  }
+  const size_t vb = dtype == BM_F64 ? 16 : 8;
+  const int forced = debug_override(BM_DBG_FFT_PATH);
+  if (sp->p.m > 0 && forced != 2 && forced != 3) {
+    const int lstride = (int)n + 1;  // odd stride: lanes on different banks
+    int L = 1;
+    auto smem_of = [&](int l) {
+      return dtype == BM_F64 ? lane_smem<double>(sp->p, l, lstride)
+                             : lane_smem<float>(sp->p, l, lstride);
+    };
+    while (L < 16 && 2 * L <= inner && smem_of(2 * L) <= kLaneSmemMulti) L *= 2;
+    if (smem_of(L) <= kLaneSmemMax) {
+      sp->path = kPathLane;
+      sp->L = L;
+      sp->lstride = lstride;
+      sp->smem = smem_of(L);
+      return BM_OK;
+    }
+  }
+  (void)vb;
+  if (sp->p.m > 0 && forced != 3) {
+    sp->path = kPathGlobal;
+    return BM_OK;
+  }
+  sp->path = kPathBluestein;
+  int64_t M = 1;
+  while (M < 2 * n - 1) M <<= 1;
+  sp->M = M;
+  sp->pm = make_plan(M);
+  const int64_t lanes = outer * inner;
+  int64_t lc = kBluesteinWorkBytes / (M * 16);
+  sp->LC = lc < 1 ? 1 : (lc > lanes ? lanes : lc);
+  return BM_OK;
+}
+
+enum { kOpAnalytic = 0, kOpEnvelopePeak = 1, kOpEnvelopeDisplay = 2 };
+
+static size_t bluestein_ws(const SigPlan& sp, int64_t n) {
+  return align256((size_t)n * 16) + align256((size_t)sp.M * 16) + align256((size_t)sp.LC * sp.M * 16);
+}
+
+// Occupancy-limited capacity of the fused kernel, or 0 if it cannot run.
+template <typename K>
+static int64_t coop_capacity(K kernel, size_t smem) {
+  int dev = 0, coop = 0, nb = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return 0;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, 256, smem) != cudaSuccess) return 0;
+  return (int64_t)nb * sm_count();
+}
 
 template <int MODE>
-static int launch_reg_f32(const float* x, float* out, unsigned* peak, int64_t outer, int64_t n,
-                          int64_t inner, cudaStream_t s) {
-  const char* e = getenv("BM_FFT_KERNEL");  // "smem": the radix-2 shared-memory kernel
-  if (e && !strcmp(e, "smem")) return -1;
-  if (n != 256 && n != 512 && n != 1024) return -1;
-  if (inner > ((int64_t)1 << 34) || outer > 65535) return -1;
-  const size_t tile = (size_t)n * 9 * (MODE == kComplex ? 8 : 4);
-  const size_t smem = (size_t)n * 8 + tile;
-  auto k = n == 256 ? analytic_reg_kernel<MODE, 8>
-                    : (n == 512 ? analytic_reg_kernel<MODE, 16> : analytic_reg_kernel<MODE, 32>);
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return BM_ERR_CUDA;
-  dim3 grid((unsigned)((inner + 7) / 8), (unsigned)outer);
-  k<<<grid, 256, smem, s>>>(x, out, peak, inner);
-  return cuda_status();
+static auto reg_kernel_for(int64_t n) {
+  return n == 256 ? analytic_reg_kernel<MODE, 8>
+                  : (n == 512 ? analytic_reg_kernel<MODE, 16> : analytic_reg_kernel<MODE, 32>);
 }
-template <>
-int launch_analytic_reg<float, kEnvelope>(const float* x, float* out, unsigned* peak, int64_t outer,
-                                          int64_t n, int64_t inner, cudaStream_t s) {
-  return launch_reg_f32<kEnvelope>(x, out, peak, outer, n, inner, s);
+static size_t reg_smem(int mode, int64_t n) {
+  const size_t nb = mode == kDisplay ? 2 : 1, tile = (size_t)n * 17;
+  return (size_t)n * 8 + nb * tile * 4 + 16;
 }
-template <>
-int launch_analytic_reg<float, kComplex>(const float* x, float* out, unsigned* peak, int64_t outer,
-                                         int64_t n, int64_t inner, cudaStream_t s) {
-  return launch_reg_f32<kComplex>(x, out, peak, outer, n, inner, s);
+constexpr int kRegCols = 16;  // columns per item of the register kernel
+
+// Items per frame and the fused-display grid, or 0 when the fused kernel
+// cannot run for this shape (the launcher then runs envelope + display).
+static int64_t fused_grid(int32_t dtype, const SigPlan& sp, int64_t n_frames, int64_t n_x,
+                          int64_t* per_frame) {
+  if (sp.path == kPathReg) {
+    *per_frame = (n_x + kRegCols - 1) / kRegCols;
+    const int64_t cap = coop_capacity(reg_kernel_for<kDisplay>(sp.p.n), reg_smem(kDisplay, sp.p.n));
+    // with one CTA per SM nothing hides a CTA's wait for its frame: measured
+    // slower than envelope + display as two launches (cfg3, n = 1024)
+    if (cap < *per_frame || cap < 2LL * sm_count()) return 0;
+    const int64_t items = n_frames * *per_frame;
+    int64_t g = (cap / *per_frame) * *per_frame;  // whole frames per round
+    return g < items ? g : items;
+  }
+  if (sp.path == kPathLane && debug_override(BM_DBG_FFT_PATH) == 1) {
+    // the shared-memory kernel holds one item at a time: its fused form
+    // measured slower than two launches (sta-paper, n = 2048), so it runs
+    // only when selected explicitly (tests)
+    *per_frame = (n_x + sp.L - 1) / sp.L;
+    const int64_t cap = dtype == BM_F64
+                            ? coop_capacity(analytic_lane_kernel<double, kDisplay>, sp.smem)
+                            : coop_capacity(analytic_lane_kernel<float, kDisplay>, sp.smem);
+    if (cap < *per_frame) return 0;
+    const int64_t items = n_frames * *per_frame;
+    int64_t g = (cap / *per_frame) * *per_frame;
+    return g < items ? g : items;
+  }
+  return 0;
+}
+
+static size_t sig_ws_bytes(int32_t dtype, int op, int64_t outer, int64_t n, int64_t inner) {
+  SigPlan sp;
+  if (sig_plan(dtype, n, outer, inner, &sp) != BM_OK) return 0;
+  const size_t vb = dtype == BM_F64 ? 16 : 8;
+  size_t b = 0;
+  if (op == kOpEnvelopeDisplay) b += align256((size_t)outer * sizeof(int));  // frame counters
+  if (sp.path == kPathBluestein) b += bluestein_ws(sp, n);
+  else if (sp.path == kPathGlobal && op != kOpAnalytic) b += align256((size_t)outer * n * inner * vb);
+  return b;
 }
 
 template <typename T, int MODE>
 static int launch_analytic(const T* x, T* out, typename PeakBits<T>::U* peak, int64_t outer,
-                           int64_t n, int64_t inner, cudaStream_t s) {
+                           int64_t n, int64_t inner, void* ws, int64_t ws_bytes, cudaStream_t s) {
   using V = typename C2<T>::type;
-  if (outer > 65535) return BM_ERR_UNSUPPORTED;
-  {
-    const int rc = launch_analytic_reg<T, MODE>(x, out, peak, outer, n, inner, s);
-    if (rc >= 0) return rc;
+  SigPlan sp;
+  const int32_t dtype = sizeof(T) == 8 ? BM_F64 : BM_F32;
+  int rc = sig_plan(dtype, n, outer, inner, &sp);
+  if (rc) return rc;
+  const int op = MODE == kComplex ? kOpAnalytic : kOpEnvelopePeak;
+  if ((size_t)ws_bytes < sig_ws_bytes(dtype, op, outer, n, inner) ||
+      (sig_ws_bytes(dtype, op, outer, n, inner) && !ws))
+    return BM_ERR_INVALID_ARGUMENT;
+  const DispArgs none{nullptr, nullptr, 0.0};
+  if (sp.path == kPathReg) {
+    if constexpr (sizeof(T) == 4) {
+      auto k = reg_kernel_for<MODE>(n);
+      const size_t smem = reg_smem(MODE, n);
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return BM_ERR_CUDA;
+      const int64_t per = (inner + kRegCols - 1) / kRegCols, items = outer * per;
+      const int64_t g = std::min<int64_t>(items, 4LL * sm_count());
+      k<<<(unsigned)g, 256, smem, s>>>(x, out, peak, items, per, inner, none);
+      return cuda_status();
+    }
+    return BM_ERR_UNSUPPORTED;
   }
-  if (is_pow2(n)) {
-    if (n > (1 << 20) || inner > (int64_t)1 << 40) return BM_ERR_UNSUPPORTED;
-    const size_t lane_bytes = (size_t)n * sizeof(V);
-    const size_t tw_bytes = (size_t)(n / 2) * sizeof(V);
-    // lanes per CTA: a power of two, enough for 32 B row segments when the
-    // image is wide, few enough to give >= 2 waves of CTAs
-    int log2L = 0;
-    while ((2 << log2L) <= 8 && (2 << log2L) <= inner &&
-           tw_bytes + (size_t)(2 << log2L) * lane_bytes <= 96 * 1024)
-      ++log2L;
-    const size_t smem = tw_bytes + ((size_t)1 << log2L) * lane_bytes;
-    if (smem > 220 * 1024) return BM_ERR_UNSUPPORTED;
-    auto k = analytic_pow2_kernel<T, MODE>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (sp.path == kPathLane) {
+    auto k = analytic_lane_kernel<T, MODE>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem) != cudaSuccess)
       return BM_ERR_CUDA;
-    const int64_t L = (int64_t)1 << log2L;
-    dim3 grid((unsigned)((inner + L - 1) / L), (unsigned)outer);
-    k<<<grid, 256, smem, s>>>(x, out, peak, (int)n, ilog2(n), inner, log2L);
-  } else {
-    const size_t smem = (size_t)n * sizeof(V) + (size_t)(n / 2 + 1) * sizeof(V) + (size_t)n * sizeof(T);
-    if (smem > 220 * 1024 || inner > 0x7fffffff) return BM_ERR_UNSUPPORTED;
-    auto k = analytic_dft_kernel<T, MODE>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return BM_ERR_CUDA;
-    dim3 grid((unsigned)inner, (unsigned)outer);
-    k<<<grid, 256, smem, s>>>(x, out, peak, n, inner);
+    const int64_t per = (inner + sp.L - 1) / sp.L, items = outer * per;
+    const int64_t g = std::min<int64_t>(items, 8LL * sm_count());
+    k<<<(unsigned)g, 256, sp.smem, s>>>(x, out, peak, sp.p, items, per, inner, sp.L, sp.lstride, none);
+    return cuda_status();
+  }
+  if (sp.path == kPathGlobal) {
+    V* buf = MODE == kComplex ? reinterpret_cast<V*>(out) : reinterpret_cast<V*>(ws);
+    const GLay lay{outer, n, inner};
+    g_load_kernel<T><<<g_blocks(outer * n * inner), 256, 0, s>>>(x, buf, lay);
+    if ((rc = g_fft<T>(buf, lay, sp.p, false, s))) return rc;
+    g_gain_kernel<T><<<g_blocks(outer * n * inner), 256, 0, s>>>(buf, lay, sp.p);
+    if ((rc = g_fft<T>(buf, lay, sp.p, true, s))) return rc;
+    dim3 grid(std::max(1u, g_blocks(n * inner) / 4), (unsigned)std::min<int64_t>(outer, 65535));
+    g_out_kernel<T, MODE><<<grid, 256, 0, s>>>(buf, out, peak, lay, T(1) / T(n));
+    return cuda_status();
+  }
+  // Bluestein
+  char* w = reinterpret_cast<char*>(ws);
+  double2* c = reinterpret_cast<double2*>(w);
+  double2* bh = reinterpret_cast<double2*>(w + align256((size_t)n * 16));
+  double2* work = reinterpret_cast<double2*>(w + align256((size_t)n * 16) + align256((size_t)sp.M * 16));
+  const int64_t M = sp.M;
+  bs_chirp_kernel<<<g_blocks(n), 256, 0, s>>>(c, n);
+  bs_bprep_kernel<<<g_blocks(M), 256, 0, s>>>(bh, c, n, M);
+  if ((rc = g_fft<double>(bh, GLay{1, M, 1}, sp.pm, false, s))) return rc;
+  const GLay xl{outer, n, inner};
+  const int64_t lanes = outer * inner;
+  for (int64_t c0 = 0; c0 < lanes; c0 += sp.LC) {
+    const int64_t lc = std::min<int64_t>(sp.LC, lanes - c0);
+    const GLay wl{1, M, lc};
+    const unsigned gb = g_blocks(lc * M);
+    bs_load_kernel<T><<<gb, 256, 0, s>>>(work, x, c, xl, c0, lc, M);
+    for (int pass = 0; pass < 2; ++pass) {
+      if ((rc = g_fft<double>(work, wl, sp.pm, false, s))) return rc;
+      bs_mulb_kernel<<<gb, 256, 0, s>>>(work, bh, lc, M);
+      if ((rc = g_fft<double>(work, wl, sp.pm, true, s))) return rc;
+      if (pass == 0) bs_mid_kernel<<<gb, 256, 0, s>>>(work, c, n, lc, M);
+    }
+    bs_out_kernel<T, MODE><<<g_blocks(lc * n), 256, 0, s>>>(work, c, out, peak, xl, c0, lc, M);
   }
   return cuda_status();
+}
+
+// K2 + K3 fused over n_frames [n_z][n_x] images (falls back to envelope into
+// disp, then display in place, where the fused kernel does not apply).
+template <typename T>
+static int launch_envelope_display(const T* x, T* disp, typename PeakBits<T>::U* peak,
+                                   int32_t* status, int64_t n_frames, int64_t n_z, int64_t n_x,
+                                   double range_db, void* ws, int64_t ws_bytes, cudaStream_t s);
+
+template <typename T>
+__global__ void envelope_kernel(const T* __restrict__ z, T* __restrict__ e, int64_t count) {
+  using V = typename C2<T>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const V v = reinterpret_cast<const V*>(z)[i];
+    e[i] = magnitude(v.x, v.y);
+  }
+}
+
+template <typename T>
+__global__ void abs_kernel(const T* __restrict__ x, T* __restrict__ e, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    e[i] = fabs(x[i]);
+}
+
+template <typename T>
+__global__ void peak_kernel(const T* __restrict__ e, typename PeakBits<T>::U* __restrict__ peak,
+                            int64_t frame_elems) {
+  const int64_t f = blockIdx.y;
+  const T* ef = e + f * frame_elems;
+  T vmax = T(0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
+       i += (int64_t)gridDim.x * blockDim.x)
+    vmax = nan_max(ef[i], vmax);
+  block_peak<T>(vmax, peak + f);
+}
+
+template <typename T>
+__global__ void display_kernel(const T* e, const typename PeakBits<T>::U* __restrict__ peak,
+                               T* disp, int32_t* __restrict__ status,
+                               int64_t frame_elems, double range_db) {
+  const int64_t f = blockIdx.y;
+  const T pk = PeakBits<T>::value(peak[f]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && status) status[f] = pk > T(0) ? 0 : 1;
+  const DispConst<T> dc(range_db);
+  const T cut = dc.q0 * pk;
+  const T* ef = e + f * frame_elems;
+  T* df = disp + f * frame_elems;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < frame_elems;
+       i += (int64_t)gridDim.x * blockDim.x)
+    df[i] = display_value_cut<T>(ef[i], pk, dc.r, cut);
+}
+
+// Column tiles of one frame gathered from the ranks of a lateral split
+// (parallel.LateralSplit): tile t holds the envelope of columns
+// [col0(t), col0(t) + w(t)) as [n_z][w(t)] at its start and the rank's peak
+// bits in its last element; widths follow frame_partition (the first
+// n_x % n_tiles tiles one column wider).  The global peak (NaN wins) is the
+// max over the tiles' peaks; every output pixel is mapped with it.
+template <typename T>
+__global__ void display_tiles_kernel(const T* __restrict__ tiles, int n_tiles, int64_t tile_stride,
+                                     int64_t n_z, int64_t n_x, T* __restrict__ disp,
+                                     int32_t* __restrict__ status, double range_db) {
+  using U = typename PeakBits<T>::U;
+  __shared__ T s_pk;
+  if (threadIdx.x == 0) {
+    T pk = T(0);
+    for (int t = 0; t < n_tiles; ++t)
+      pk = nan_max(PeakBits<T>::value(reinterpret_cast<const U*>(tiles + t * tile_stride)[tile_stride - 1]), pk);
+    s_pk = pk;
+    if (blockIdx.x == 0 && status) *status = pk > T(0) ? 0 : 1;
+  }
+  __syncthreads();
+  const T pk = s_pk;
+  const DispConst<T> dc(range_db);
+  const int64_t base = n_x / n_tiles, extra = n_x % n_tiles, wide = extra * (base + 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_z * n_x;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i / n_x, x = i - z * n_x;
+    const int64_t t = x < wide ? x / (base + 1) : extra + (x - wide) / base;
+    const int64_t w = base + (t < extra ? 1 : 0), c0 = t * base + (t < extra ? t : extra);
+    disp[i] = display_value_cut<T>(tiles[t * tile_stride + z * w + (x - c0)], pk, dc.r, dc.q0 * pk);
+  }
 }
 
 static inline int grid_for(int64_t count) {
@@ -540,19 +981,95 @@ static inline int grid_for(int64_t count) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+template <typename T>
+static int launch_display(const T* e, const typename PeakBits<T>::U* peak, T* disp, int32_t* status,
+                          int64_t n_frames, int64_t frame_elems, double range_db, cudaStream_t s) {
+  int gx = grid_for(frame_elems);
+  if (gx > 2 * sm_count()) gx = 2 * sm_count();
+  for (int64_t f0 = 0; f0 < n_frames; f0 += 65535) {
+    const int64_t nf = std::min<int64_t>(65535, n_frames - f0);
+    display_kernel<T><<<dim3(gx, (unsigned)nf), 256, 0, s>>>(
+        e + f0 * frame_elems, peak + f0, disp + f0 * frame_elems, status ? status + f0 : nullptr,
+        frame_elems, range_db);
+  }
+  return cuda_status();
+}
+
+template <typename T>
+static int launch_envelope_display(const T* x, T* disp, typename PeakBits<T>::U* peak,
+                                   int32_t* status, int64_t n_frames, int64_t n_z, int64_t n_x,
+                                   double range_db, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  const int32_t dtype = sizeof(T) == 8 ? BM_F64 : BM_F32;
+  SigPlan sp;
+  int rc = sig_plan(dtype, n_z, n_frames, n_x, &sp);
+  if (rc) return rc;
+  const size_t need = sig_ws_bytes(dtype, kOpEnvelopeDisplay, n_frames, n_z, n_x);
+  if (!ws || (size_t)ws_bytes < need) return BM_ERR_INVALID_ARGUMENT;
+  int* done = reinterpret_cast<int*>(ws);
+  const size_t cnt_bytes = align256((size_t)n_frames * sizeof(int));
+  if (cudaMemsetAsync(peak, 0, sizeof(typename PeakBits<T>::U) * n_frames, s) != cudaSuccess)
+    return BM_ERR_CUDA;
+  int64_t per_frame = 0;
+  const int64_t g = debug_override(BM_DBG_NO_FUSED_DISPLAY) > 0
+                        ? 0 : fused_grid(dtype, sp, n_frames, n_x, &per_frame);
+  if (g > 0) {
+    if (cudaMemsetAsync(done, 0, (size_t)n_frames * sizeof(int), s) != cudaSuccess) return BM_ERR_CUDA;
+    DispArgs da{status, done, range_db};
+    int64_t items = n_frames * per_frame, inner = n_x;
+    const T* xa = x;
+    T* oa = disp;
+    auto* pa = peak;
+    if (sp.path == kPathReg) {
+      if constexpr (sizeof(T) == 4) {
+        auto k = reg_kernel_for<kDisplay>(n_z);
+        void* args[] = {(void*)&xa, (void*)&oa, (void*)&pa, (void*)&items, (void*)&per_frame,
+                        (void*)&inner, (void*)&da};
+        if (cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)g), dim3(256), args,
+                                        reg_smem(kDisplay, n_z), s) != cudaSuccess)
+          return BM_ERR_CUDA;
+        return cuda_status();
+      }
+    } else {
+      auto k = analytic_lane_kernel<T, kDisplay>;
+      FftPlan p = sp.p;
+      int L = sp.L, ls = sp.lstride;
+      void* args[] = {(void*)&xa, (void*)&oa, (void*)&pa, (void*)&p, (void*)&items,
+                      (void*)&per_frame, (void*)&inner, (void*)&L, (void*)&ls, (void*)&da};
+      if (cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)g), dim3(256), args, sp.smem,
+                                      s) != cudaSuccess)
+        return BM_ERR_CUDA;
+      return cuda_status();
+    }
+  }
+  // envelope + peak into disp, then the display mapping in place
+  char* w = reinterpret_cast<char*>(ws) + cnt_bytes;
+  rc = launch_analytic<T, kEnvelope>(x, disp, peak, n_frames, n_z, n_x, w,
+                                     (int64_t)(need - cnt_bytes), s);
+  if (rc) return rc;
+  return launch_display<T>(disp, peak, disp, status, n_frames, n_z * n_x, range_db, s);
+}
+
 }  // namespace bm
 
 using namespace bm;
 
+extern "C" int64_t bm_sigproc_ws_bytes(int32_t op, int32_t dtype, int64_t outer, int64_t n,
+                                       int64_t inner) {
+  if ((dtype != BM_F32 && dtype != BM_F64) || op < 0 || op > 2 || n < 2) return 0;
+  return (int64_t)sig_ws_bytes(dtype, op, outer, n, inner);
+}
+
 extern "C" int bm_analytic_signal(int32_t dtype, const void* x, void* z, int64_t outer, int64_t n,
-                                  int64_t inner, void* stream) {
+                                  int64_t inner, void* ws, int64_t ws_bytes, void* stream) {
   if (!x || !z || outer < 1 || inner < 1) return BM_ERR_INVALID_ARGUMENT;
   if (n < 2) return BM_ERR_AXIS_TOO_SHORT;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == BM_F32)
-    return launch_analytic<float, kComplex>((const float*)x, (float*)z, nullptr, outer, n, inner, s);
+    return launch_analytic<float, kComplex>((const float*)x, (float*)z, nullptr, outer, n, inner,
+                                            ws, ws_bytes, s);
   if (dtype == BM_F64)
-    return launch_analytic<double, kComplex>((const double*)x, (double*)z, nullptr, outer, n, inner, s);
+    return launch_analytic<double, kComplex>((const double*)x, (double*)z, nullptr, outer, n, inner,
+                                             ws, ws_bytes, s);
   return BM_ERR_INVALID_ARGUMENT;
 }
 
@@ -569,8 +1086,22 @@ extern "C" int bm_envelope(int32_t dtype, const void* z, void* e, int64_t count,
   return cuda_status();
 }
 
+extern "C" int bm_abs(int32_t dtype, const void* x, void* e, int64_t count, void* stream) {
+  if (!x || !e || count < 0) return BM_ERR_INVALID_ARGUMENT;
+  if (count == 0) return BM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == BM_F32)
+    abs_kernel<float><<<grid_for(count), 256, 0, s>>>((const float*)x, (float*)e, count);
+  else if (dtype == BM_F64)
+    abs_kernel<double><<<grid_for(count), 256, 0, s>>>((const double*)x, (double*)e, count);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}
+
 extern "C" int bm_envelope_peak(int32_t dtype, const void* rf_img, void* env, void* peak,
-                                int32_t n_frames, int64_t n_z, int64_t n_x, void* stream) {
+                                int32_t n_frames, int64_t n_z, int64_t n_x, void* ws,
+                                int64_t ws_bytes, void* stream) {
   if (!rf_img || !env || !peak || n_frames < 1 || n_x < 1) return BM_ERR_INVALID_ARGUMENT;
   if (n_z < 2) return BM_ERR_AXIS_TOO_SHORT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -578,11 +1109,48 @@ extern "C" int bm_envelope_peak(int32_t dtype, const void* rf_img, void* env, vo
   if (cudaMemsetAsync(peak, 0, pb * n_frames, s) != cudaSuccess) return BM_ERR_CUDA;
   if (dtype == BM_F32)
     return launch_analytic<float, kEnvelope>((const float*)rf_img, (float*)env,
-                                             (unsigned int*)peak, n_frames, n_z, n_x, s);
+                                             (unsigned int*)peak, n_frames, n_z, n_x, ws, ws_bytes, s);
   if (dtype == BM_F64)
     return launch_analytic<double, kEnvelope>((const double*)rf_img, (double*)env,
-                                              (unsigned long long*)peak, n_frames, n_z, n_x, s);
+                                              (unsigned long long*)peak, n_frames, n_z, n_x, ws,
+                                              ws_bytes, s);
   return BM_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int bm_envelope_display(int32_t dtype, const void* rf_img, void* disp, void* peak,
+                                   int32_t* status, int32_t n_frames, int64_t n_z, int64_t n_x,
+                                   double range_db, void* ws, int64_t ws_bytes, void* stream) {
+  if (!rf_img || !disp || !peak || n_frames < 1 || n_x < 1) return BM_ERR_INVALID_ARGUMENT;
+  if (!(range_db > 0) || range_db != range_db) return BM_ERR_INVALID_ARGUMENT;
+  if (n_z < 2) return BM_ERR_AXIS_TOO_SHORT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == BM_F32)
+    return launch_envelope_display<float>((const float*)rf_img, (float*)disp, (unsigned*)peak,
+                                          status, n_frames, n_z, n_x, range_db, ws, ws_bytes, s);
+  if (dtype == BM_F64)
+    return launch_envelope_display<double>((const double*)rf_img, (double*)disp,
+                                           (unsigned long long*)peak, status, n_frames, n_z, n_x,
+                                           range_db, ws, ws_bytes, s);
+  return BM_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int bm_display_tiles(int32_t dtype, const void* tiles, int32_t n_tiles,
+                                int64_t tile_stride, int64_t n_z, int64_t n_x, void* disp,
+                                int32_t* status, double range_db, void* stream) {
+  if (!tiles || !disp || n_tiles < 1 || n_z < 1 || n_x < n_tiles) return BM_ERR_INVALID_ARGUMENT;
+  if (tile_stride < n_z * ((n_x + n_tiles - 1) / n_tiles) + 1) return BM_ERR_INVALID_ARGUMENT;
+  if (!(range_db > 0) || range_db != range_db) return BM_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = grid_for(n_z * n_x);
+  if (dtype == BM_F32)
+    display_tiles_kernel<float><<<g, 256, 0, s>>>((const float*)tiles, n_tiles, tile_stride, n_z,
+                                                  n_x, (float*)disp, status, range_db);
+  else if (dtype == BM_F64)
+    display_tiles_kernel<double><<<g, 256, 0, s>>>((const double*)tiles, n_tiles, tile_stride, n_z,
+                                                   n_x, (double*)disp, status, range_db);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
 }
 
 extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
@@ -608,22 +1176,16 @@ extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n
 extern "C" int bm_display(int32_t dtype, const void* e, const void* peak, void* disp,
                           int32_t* status, int32_t n_frames, int64_t frame_elems, double range_db,
                           void* stream) {
-  if (!e || !peak || !disp || n_frames < 1 || n_frames > 65535 || frame_elems < 0)
-    return BM_ERR_INVALID_ARGUMENT;
+  if (!e || !peak || !disp || n_frames < 1 || frame_elems < 0) return BM_ERR_INVALID_ARGUMENT;
   if (!(range_db > 0) || range_db != range_db) return BM_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
-  int gx = grid_for(frame_elems);
-  if (gx > 2 * sm_count()) gx = 2 * sm_count();
-  dim3 grid(gx, n_frames);
   if (dtype == BM_F32)
-    display_kernel<float><<<grid, 256, 0, s>>>((const float*)e, (const unsigned int*)peak,
-                                              (float*)disp, status, frame_elems, range_db);
-  else if (dtype == BM_F64)
-    display_kernel<double><<<grid, 256, 0, s>>>((const double*)e, (const unsigned long long*)peak,
-                                               (double*)disp, status, frame_elems, range_db);
-  else
-    return BM_ERR_INVALID_ARGUMENT;
-  return cuda_status();
+    return launch_display<float>((const float*)e, (const unsigned*)peak, (float*)disp, status,
+                                 n_frames, frame_elems, range_db, s);
+  if (dtype == BM_F64)
+    return launch_display<double>((const double*)e, (const unsigned long long*)peak, (double*)disp,
+                                  status, n_frames, frame_elems, range_db, s);
+  return BM_ERR_INVALID_ARGUMENT;
 }
 
 extern "C" int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
@@ -646,6 +1208,16 @@ extern "C" const char* bm_error_string(int code) {
 }
 
 extern "C" int bm_abi_version(void) { return BMODE200_ABI_VERSION; }
+
+extern "C" int bm_debug_set(int32_t key, int32_t value) {
+  if (key < 0 || key >= BM_DBG_COUNT) return 0;
+  return bm::g_debug_overrides[key].exchange(value);
+}
+
+extern "C" int bm_debug_get(int32_t key) {
+  if (key < 0 || key >= BM_DBG_COUNT) return 0;
+  return bm::debug_override(key);
+}
 
 // Display -> 8-bit pixels for PGM output (formats.py:189-200):
 // floor(v * 255 + 0.5) with each operator rounded in the display dtype, as

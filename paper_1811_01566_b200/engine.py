@@ -7,8 +7,9 @@ streams of frames that share one acquisition geometry -- BASELINE config 4,
 
     das_beamform -> analytic_signal -> envelope -> dynamic_adjustment
 
-on a batch of frames with three launches (``bm_das_beamform``,
-``bm_envelope_peak``, ``bm_display``) and, for host-resident input, overlaps
+on a batch of frames with two launches (``bm_das_beamform`` and the fused
+``bm_envelope_display``: FFT -> gain -> IFFT -> |.| -> per-frame max -> dB,
+the envelope kept on chip) and, for host-resident input, overlaps
 the host->device copy of chunk i+1 and the device->host copy of chunk i-1
 with the reconstruction of chunk i (SURVEY §8(f) "next #1": RF ingest).
 
@@ -60,11 +61,14 @@ class BmodeEngine:
         if cur is None or cur[0] < n_frames:
             nz, nx = self.image_shape
             rf_img = torch.empty((n_frames, nz, nx), dtype=self.tdtype, device=self.device)
-            env = torch.empty_like(rf_img)
             peak = torch.empty(n_frames, dtype=torch.int32 if self.code == N.BM_F32 else torch.int64,
                                device=self.device)
             status = torch.zeros(n_frames, dtype=torch.int32, device=self.device)
-            cur = (n_frames, rf_img, env, peak, status)
+            with torch.cuda.device(self.device):
+                nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_DISPLAY, self.code, n_frames,
+                                                      nz, nx))
+            ws = N.workspace(nb, self.device)
+            cur = (n_frames, rf_img, ws, peak, status, nb)
             self._ws[key] = cur
         return cur
 
@@ -75,8 +79,8 @@ class BmodeEngine:
         import torch
 
         f = int(rf.shape[0])
-        _, rf_img, env, peak, st = self._buffers(f, key)
-        rf_img, env, peak = rf_img[:f], env[:f], peak[:f]
+        _, rf_img, ws, peak, st, nb = self._buffers(f, key)
+        rf_img, peak = rf_img[:f], peak[:f]
         status = st[:f] if status is None else status
         if out is None:
             out = torch.empty((f,) + self.image_shape, dtype=self.tdtype, device=self.device)
@@ -87,11 +91,10 @@ class BmodeEngine:
         if das_events is not None:
             das_events[1].record(stream)
         nz, nx = self.image_shape
-        N.call("bm_envelope_peak", self.code, rf_img.data_ptr(), env.data_ptr(), peak.data_ptr(),
-               f, nz, nx, s)
-        N.call("bm_display", self.code, env.data_ptr(), peak.data_ptr(), out.data_ptr(),
-               status.data_ptr(), f, nz * nx, self.range_db, s)
-        self.launches += 3
+        with torch.cuda.device(self.device):
+            N.call("bm_envelope_display", self.code, rf_img.data_ptr(), out.data_ptr(),
+                   peak.data_ptr(), status.data_ptr(), f, nz, nx, self.range_db, ws.data_ptr(), nb, s)
+        self.launches += 2
         if not isinstance(key, tuple):
             self._last_status = status
         return out

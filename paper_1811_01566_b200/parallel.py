@@ -1,30 +1,38 @@
 """Multi-GPU partitioning of the B-mode path.
 
-Two cases, one process per GPU (torch.distributed, NCCL on GPUs, gloo in
-the CPU tests):
+One process per GPU (torch.distributed; NCCL on GPUs, gloo in the CPU tests):
 
 * **Independent frames** (config 4, cine streams): `frame_partition` deals
   frames to ranks; there is no data-path collective.
 
-* **One large frame** (config 5, 2048 x 2048 STAI): `LateralSplit` gives
-  every rank a contiguous slab of image COLUMNS at all depths.  Delay-and-
-  Sum is per pixel, so each rank's slab is bitwise equal to the same columns
-  of a single-GPU run; the analytic signal runs along depth, so every FFT
-  lane is rank-local.  The only coupling is the per-frame peak of
-  dynamic_adjustment (sigproc.py:90): one all-reduce(MAX) of a single
-  float, then each rank maps its slab to display values and one gather
-  assembles the B-mode image on the destination rank.
+* **One large frame** (config 5, 2048 x 2048 STAI), `LateralSplit`: every
+  rank owns a contiguous slab of image COLUMNS at all depths.  Delay-and-Sum
+  is per pixel, so a rank's slab is bitwise the same columns of a one-GPU
+  run, and the analytic signal runs along depth, so every FFT lane is
+  rank-local.  Per frame a rank runs two of its own kernels and ONE
+  collective:
+
+    1. ``bm_das_beamform`` of its slab;
+    2. ``bm_envelope_peak`` writing the slab's envelope AND its peak straight
+       into the rank's send tile [envelope (n_z x w) | ... | peak bits];
+    3. ``dist.gather`` of the tiles to ``dst`` (NCCL);
+
+  and ``dst`` alone maps the stitched frame with ``bm_display_tiles`` (global
+  peak = max of the tiles' peaks, read on the device).  No host
+  synchronisation, no torch reductions, no concatenation copies.  AllZeroInput
+  (sigproc.py:91-92) is raised on ``dst`` from the kernel's status word after
+  the gather, so no rank can be left waiting in a collective.
 
 * **One large frame, split by depth ROWS** (`RowSplit`, the north star's
   literal "image rows are split across GPUs"): each rank beamforms a band of
-  rows at all columns -- again bitwise the same pixels as one GPU -- but a
-  band cuts every axial FFT lane, so the beamformed RF bands are gathered
-  to the destination rank, which runs the envelope + display of the whole
-  frame (the same kernels as one GPU, so the same bits).  One all-gather of
-  f32 RF rows, no other collective.
+  rows at all columns -- bitwise the same pixels as one GPU -- but a band cuts
+  every axial FFT lane, so the bands are gathered to ``dst`` (one gather of
+  f32 RF rows), which runs the fused envelope + display of the whole frame
+  (the same kernel as one GPU, so the same bits).
 
-The per-rank compute is injectable (`local_fn(sub_grid, rank) -> envelope
-slab`) so the partition/collective logic is testable on CPU with gloo.
+The collective and packing logic is plain torch.distributed over tensors,
+so it runs (and is tested) with gloo on CPU tensors; the device kernels are
+only called on CUDA tensors.
 """
 
 from __future__ import annotations
@@ -42,8 +50,15 @@ def frame_partition(n_frames: int, world: int, rank: int) -> range:
 
 
 def column_slabs(n_x: int, world: int) -> list[tuple[int, int]]:
-    """[lo, hi) column ranges, one per rank, sizes differing by <= 1."""
+    """[lo, hi) column ranges, one per rank, sizes differing by <= 1 (the
+    first n_x % world one wider -- the layout bm_display_tiles assumes)."""
     return [(r.start, r.stop) for r in (frame_partition(n_x, world, k) for k in range(world))]
+
+
+def _peak_dtype(dtype):
+    import torch
+
+    return torch.int32 if dtype == torch.float32 else torch.int64
 
 
 class LateralSplit:
@@ -59,62 +74,74 @@ class LateralSplit:
         self.sub_grid = ImageGrid(np.asarray(grid.x_positions)[lo:hi],
                                   np.asarray(grid.z_positions))
 
-    def pad_width(self) -> int:
-        return max(h - l for l, h in self.slabs)
+    @property
+    def tile_stride(self) -> int:
+        """Elements per tile: the widest slab's envelope plus one peak slot."""
+        return self.grid.n_z * max(h - l for l, h in self.slabs) + 1
 
-    def display(self, env_slab, range_db: float, group=None, dst: int = 0):
-        """Global-peak dB mapping of this rank's envelope slab, gathered to
-        `dst`.  `env_slab` is a torch tensor [n_z, n_cols] (CUDA with NCCL,
-        CPU with gloo).  Returns the full [n_z, n_x] display on `dst`, None
-        elsewhere."""
+    def send_tile(self, dtype, device):
         import torch
-        import torch.distributed as dist
 
-        peak = env_slab.max().reshape(1).to(torch.float64)
-        dist.all_reduce(peak, op=dist.ReduceOp.MAX, group=group)
-        disp = map_display(env_slab, float(peak.item()), range_db)
-        return self.gather(disp, group=group, dst=dst)
+        return torch.zeros(self.tile_stride, dtype=dtype, device=device)
 
-    def gather(self, slab, group=None, dst: int = 0):
-        """Gather equal-padded column slabs to `dst` and stitch them."""
+    def recv_tiles(self, dtype, device):
         import torch
-        import torch.distributed as dist
 
-        n_z = slab.shape[0]
-        w = self.pad_width()
-        buf = torch.zeros((n_z, w), dtype=slab.dtype, device=slab.device)
-        buf[:, : slab.shape[1]] = slab
-        parts = [torch.empty_like(buf) for _ in range(self.world)]
-        dist.all_gather(parts, buf.contiguous(), group=group)
-        if dist.get_rank(group) != dst:
-            return None
-        return torch.cat([p[:, : h - l] for p, (l, h) in zip(parts, self.slabs)], dim=1)
+        return torch.zeros((self.world, self.tile_stride), dtype=dtype, device=device)
 
+    def tile_views(self, tile):
+        """(envelope [n_z, w] view, peak-bits [1] view) of this rank's tile."""
+        return self.envelope_view(tile, self.rank), tile[-1:].view(_peak_dtype(tile.dtype))
 
-def map_display(env, peak: float, range_db: float):
-    """dB mapping of an envelope slab against a GLOBAL peak, on the device
-    that holds it: the bm_display kernel for CUDA tensors (same arithmetic as
-    the single-GPU path), torch ops for CPU tensors (gloo tests only)."""
-    import torch
+    def envelope_view(self, tile, rank: int):
+        lo, hi = self.slabs[rank]
+        return tile[: self.grid.n_z * (hi - lo)].view(self.grid.n_z, hi - lo)
 
-    if env.is_cuda:
+    def envelope_into_tile(self, rf_slab, tile):
+        """Envelope + peak of this rank's beamformed slab [n_z, w] written in
+        place into `tile` by bm_envelope_peak (CUDA)."""
+        import torch
+
         from . import _native as N
 
-        code = N.BM_F32 if env.dtype == torch.float32 else N.BM_F64
-        bits = torch.tensor([peak], dtype=env.dtype).view(
-            torch.int32 if code == N.BM_F32 else torch.int64).to(env.device)
-        out = torch.empty_like(env)
-        status = torch.empty(1, dtype=torch.int32, device=env.device)
-        e = env.contiguous()
-        N.call("bm_display", code, e.data_ptr(), bits.data_ptr(), out.data_ptr(),
-               status.data_ptr(), 1, e.numel(), float(range_db), N.stream_ptr())
-        return out
-    e = env
-    pos = e > 0
-    out = torch.zeros_like(e)
-    db = 20.0 * torch.log10(e[pos] / e.new_tensor(peak))
-    out[pos] = torch.clamp(db + range_db, 0.0, range_db) / range_db
-    return out
+        n_z, w = rf_slab.shape
+        x = rf_slab.contiguous()
+        code = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
+        env, peak = self.tile_views(tile)
+        with torch.cuda.device(x.device):
+            nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_PEAK, code, 1, n_z, w))
+            ws = N.workspace(nb, x.device)
+            N.call("bm_envelope_peak", code, x.data_ptr(), env.data_ptr(), peak.data_ptr(), 1,
+                   n_z, w, ws.data_ptr() if ws is not None else None, nb, N.stream_ptr())
+        return tile
+
+    def gather(self, tile, recv=None, group=None, dst: int = 0):
+        """THE collective: gather every rank's tile to `dst` (one row each of
+        `recv`).  Returns `recv` on dst, None elsewhere."""
+        import torch.distributed as dist
+
+        me = dist.get_rank(group)
+        dst_g = dist.get_global_rank(group, dst) if group is not None else dst
+        dist.gather(tile, gather_list=list(recv.unbind(0)) if me == dst else None, dst=dst_g,
+                    group=group)
+        return recv if me == dst else None
+
+    def display(self, recv, range_db: float, out=None):
+        """Display [n_z, n_x] of the gathered tiles (bm_display_tiles, on the
+        destination's device).  Returns (display, status)."""
+        import torch
+
+        from . import _native as N
+
+        n_z, n_x = self.grid.n_z, self.grid.n_x
+        code = N.BM_F32 if recv.dtype == torch.float32 else N.BM_F64
+        if out is None:
+            out = torch.empty((n_z, n_x), dtype=recv.dtype, device=recv.device)
+        status = torch.empty(1, dtype=torch.int32, device=recv.device)
+        with torch.cuda.device(recv.device):
+            N.call("bm_display_tiles", code, recv.data_ptr(), self.world, self.tile_stride, n_z,
+                   n_x, out.data_ptr(), status.data_ptr(), float(range_db), N.stream_ptr())
+        return out, status
 
 
 def row_bands(n_z: int, world: int) -> list[tuple[int, int]]:
@@ -135,40 +162,59 @@ class RowSplit:
         self.sub_grid = ImageGrid(np.asarray(grid.x_positions),
                                   np.asarray(grid.z_positions)[lo:hi])
 
-    def gather(self, band, group=None, dst: int = 0):
-        """Gather equal-padded row bands [rows, n_x] to `dst` and stack them."""
+    @property
+    def band_rows(self) -> int:
+        return max(b - a for a, b in self.bands)
+
+    def send_band(self, dtype, device):
+        """[band_rows, n_x] send buffer; DAS writes this rank's rows into its top."""
+        import torch
+
+        return torch.zeros((self.band_rows, self.grid.n_x), dtype=dtype, device=device)
+
+    def recv_bands(self, dtype, device):
+        import torch
+
+        return torch.zeros((self.world, self.band_rows, self.grid.n_x), dtype=dtype,
+                           device=device)
+
+    def gather(self, band, recv=None, group=None, dst: int = 0):
+        """Gather every rank's band to `dst`; returns the stitched frame
+        [n_z, n_x] there (a view when the bands are equal, else one copy),
+        None elsewhere."""
         import torch
         import torch.distributed as dist
 
-        h = max(b - a for a, b in self.bands)
-        buf = torch.zeros((h,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
-        buf[: band.shape[0]] = band
-        parts = [torch.empty_like(buf) for _ in range(self.world)]
-        dist.all_gather(parts, buf.contiguous(), group=group)
-        if dist.get_rank(group) != dst:
+        me = dist.get_rank(group)
+        dst_g = dist.get_global_rank(group, dst) if group is not None else dst
+        dist.gather(band, gather_list=list(recv.unbind(0)) if me == dst else None, dst=dst_g,
+                    group=group)
+        if me != dst:
             return None
-        return torch.cat([p[: b - a] for p, (a, b) in zip(parts, self.bands)], dim=0)
+        h = self.band_rows
+        if all(b - a == h for a, b in self.bands):
+            return recv.view(self.world * h, self.grid.n_x)
+        return torch.cat([recv[r, : b - a] for r, (a, b) in enumerate(self.bands)], dim=0)
 
 
 def envelope_display(rf_img, range_db: float):
     """Envelope + dB display of one beamformed frame [n_z, n_x] on its device
-    (the bm_envelope_peak + bm_display kernels of the single-GPU chain).
-    Returns (display, envelope)."""
+    (the fused bm_envelope_display of the single-GPU chain).  Returns
+    (display, status)."""
     import torch
 
     from . import _native as N
 
     x = rf_img.contiguous()
     code = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
-    env = torch.empty_like(x)
-    peak = torch.empty(1, dtype=torch.int32 if code == N.BM_F32 else torch.int64, device=x.device)
+    peak = torch.empty(1, dtype=_peak_dtype(x.dtype), device=x.device)
     disp = torch.empty_like(x)
     status = torch.empty(1, dtype=torch.int32, device=x.device)
     n_z, n_x = x.shape
     with torch.cuda.device(x.device):
-        N.call("bm_envelope_peak", code, x.data_ptr(), env.data_ptr(), peak.data_ptr(), 1, n_z, n_x,
+        nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_DISPLAY, code, 1, n_z, n_x))
+        ws = N.workspace(nb, x.device)
+        N.call("bm_envelope_display", code, x.data_ptr(), disp.data_ptr(), peak.data_ptr(),
+               status.data_ptr(), 1, n_z, n_x, float(range_db), ws.data_ptr(), nb,
                N.stream_ptr())
-        N.call("bm_display", code, env.data_ptr(), peak.data_ptr(), disp.data_ptr(),
-               status.data_ptr(), 1, n_z * n_x, float(range_db), N.stream_ptr())
-    return disp, env
-
+    return disp, status

@@ -132,11 +132,12 @@ def analytic_signal(x, axis: int = -1):
     inner = int(np.prod(shape[ax + 1:], dtype=np.int64))
     z = torch.empty(shape + (2,), dtype=tdt, device=dev)
     if xd.numel():
+        code = N.dtype_code(rdt)
         with torch.cuda.device(dev):
-            for o0 in range(0, outer, 65535):
-                no = min(65535, outer - o0)
-                N.call("bm_analytic_signal", N.dtype_code(rdt), xd.reshape(-1)[o0 * n * inner:].data_ptr(),
-                       z.reshape(-1)[o0 * n * inner * 2:].data_ptr(), no, n, inner, N.stream_ptr())
+            nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ANALYTIC, code, outer, n, inner))
+            ws = N.workspace(nb, dev)
+            N.call("bm_analytic_signal", code, xd.data_ptr(), z.data_ptr(), outer, n, inner,
+                   ws.data_ptr() if ws is not None else None, nb, N.stream_ptr())
     zc = torch.view_as_complex(z)
     if is_t and x.is_cuda:
         return zc
@@ -150,10 +151,8 @@ def envelope(z):
     is_t = _is_torch(z)
     if not is_t:
         z = np.asarray(z)
-        if not np.iscomplexobj(z):
-            return np.abs(z)
-    elif not z.is_complex():
-        return z.abs()
+    if not (z.is_complex() if is_t else np.iscomplexobj(z)):
+        return _abs_device(z, is_t)
     dev = z.device if is_t and z.is_cuda else _dev()
     zd = to_device(z, dev)
     rdt = torch.float32 if zd.dtype == torch.complex64 else torch.float64
@@ -165,6 +164,41 @@ def envelope(z):
         N.call("bm_envelope", N.BM_F32 if rdt == torch.float32 else N.BM_F64, zr.data_ptr(),
                e.data_ptr(), zd.numel(), N.stream_ptr())
     return e if is_t and z.is_cuda else e.cpu().numpy()
+
+
+def _abs_device(x, is_t):
+    """|x| of a real tensor on the device (np.abs of a real envelope input)."""
+    import torch
+
+    dev = x.device if is_t and x.is_cuda else _dev()
+    dt = np.dtype(_np_dtype(x))
+    if dt not in (np.float32, np.float64):
+        dt = np.dtype(np.float64)
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    xd = to_device(x, dev, tdt)
+    e = torch.empty_like(xd)
+    if xd.numel():
+        with torch.cuda.device(dev):
+            N.call("bm_abs", N.dtype_code(dt), xd.data_ptr(), e.data_ptr(), xd.numel(),
+                   N.stream_ptr())
+    return e if is_t and x.is_cuda else e.cpu().numpy()
+
+
+def envelope_peak_device(x, n_frames: int, n_z: int, n_x: int):
+    """Fused analytic -> |.| -> per-frame peak of device images ``x``
+    ([n_frames, n_z, n_x] contiguous): returns (env, peak_bits)."""
+    import torch
+
+    code = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
+    env = torch.empty_like(x)
+    peak = torch.empty(n_frames, dtype=torch.int32 if code == N.BM_F32 else torch.int64,
+                       device=x.device)
+    with torch.cuda.device(x.device):
+        nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_PEAK, code, n_frames, n_z, n_x))
+        ws = N.workspace(nb, x.device)
+        N.call("bm_envelope_peak", code, x.data_ptr(), env.data_ptr(), peak.data_ptr(), n_frames,
+               n_z, n_x, ws.data_ptr() if ws is not None else None, nb, N.stream_ptr())
+    return env, peak
 
 
 def _dyn_device(e, range_db: float, peak=None):

@@ -95,3 +95,13 @@ def chain_cases(T):
 def config_rf(shape, seed, kind="noise"):
     """Full-size synthetic RF that any box can regenerate: seeded N(0,1) f32."""
     return np.random.default_rng(seed).normal(size=shape).astype(np.float32)
+
+
+# (n, f32 lanes, f64 lanes) of the long-axis analytic-signal goldens: 37 lanes
+# leave a partial 8-lane CTA
+LONG_AXES = ((2048, 37, 5), (4096, 9, 3))
+
+
+def long_lanes(n, lanes, dtype):
+    """Seeded [n, lanes] input of the long-axis analytic-signal goldens."""
+    return np.random.default_rng(1000 + 7 * n + lanes).normal(size=(n, lanes)).astype(dtype)

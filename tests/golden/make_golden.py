@@ -25,6 +25,13 @@ Outputs:
                   with an rx map); pgm.npz: write_pgm bytes of seeded displays.
   sim.npz         simulate_rf (noise-free): f64 STA (t0, rx map) and PW frames,
                   sha256 of the cfg2 wire-phantom f32 frame.
+  engine.npz      the benchmarked batched path: per frame of the bench's own
+                  cine generator (cfg2 wire phantom + N(0, 0.01), seed = frame
+                  index; cfg1 and cfg3 likewise), the sha256 of the f32 input
+                  RF, the sha256 of the reference's das_beamform output, and
+                  the full f32 display of the reference chain for some frames.
+  sigproc_long.npz  analytic_signal at n = 2048 / 4096 (f32: 37 / 9 lanes,
+                  f64: 5 / 3 lanes; inputs from cases.long_lanes).
   configs.json    sha256 of das_beamform f32 output at full BASELINE sizes
                   (cfg1/cfg2 linear+nearest, cfg3 linear, cfg1 f64) on seeded
                   N(0,1) RF, and of simulate_rf for the cfg2 wire phantom.
@@ -260,8 +267,68 @@ def configs():
         json.dump(res, f, indent=1, sort_keys=True)
 
 
+def _ref_ctx(ctx_m):
+    return ET.AcquisitionContext(ctx_m.speed_of_sound, ctx_m.sampling_frequency,
+                                 ctx_m.n_elements, ctx_m.pitch,
+                                 ET.PwScheme(ctx_m.tx_scheme.angles_rad) if ctx_m.is_pw
+                                 else ET.StaScheme(ctx_m.tx_scheme.tx_elements))
+
+
+# frames of each config's bench cine that get golden outputs: (rf sha seeds,
+# display seeds).  cfg2 batches are 32 frames (FP = 2 x FT = 4 passes), so the
+# seeds hit several pass / thread slots; cfg3 batches are 8 frames.
+ENGINE_FRAMES = {"cfg2": ((0, 1, 2, 3, 13, 31), (0, 13, 31)),
+                 "cfg1": ((0, 5, 31), (0,)),
+                 "cfg3": ((0, 7), (0,))}
+
+
+def engine():
+    """engine.npz: reference outputs for frames of bench.synth_frames' cine
+    (the clean wire-phantom frame from the reference's own simulate_rf in f64,
+    plus N(0, 0.01) drawn from default_rng(seed), cast to f32)."""
+    from paper_1811_01566_b200 import environment as ME
+
+    out = {}
+    for name, (rf_seeds, disp_seeds) in ENGINE_FRAMES.items():
+        ctx_m, grid_m, n_s = ME.config_geometry(name)
+        ctx = _ref_ctx(ctx_m)
+        grid = ET.ImageGrid(grid_m.x_positions, grid_m.z_positions)
+        clean = EE.simulate_rf(EP.wire_phantom(), ctx, n_s, dtype=np.float64).data
+        plan = None
+        for seed in rf_seeds:
+            rng = np.random.default_rng(seed)
+            data = (clean + rng.normal(0.0, 0.01, clean.shape)).astype(np.float32)
+            frame = ET.RfFrame(data)
+            if plan is None:
+                plan = EB.DasPlan(ctx, grid, ET.ApodizationSpec(), np.float32, ctx.n_elements)
+            rf = EB.das_beamform(frame, ctx, grid, plan=plan).data
+            out[f"{name}_in_sha_{seed}"] = np.array(sha(data))
+            out[f"{name}_rf_sha_{seed}"] = np.array(sha(rf))
+            if seed in disp_seeds:
+                env = ES.envelope(ES.analytic_signal(rf, axis=0))
+                out[f"{name}_disp_{seed}"] = ES.dynamic_adjustment(env, 30.0).astype(np.float32)
+            print(name, seed, flush=True)
+    np.savez_compressed(os.path.join(HERE, "engine.npz"), **out)
+
+
+def sigproc_long():
+    """sigproc_long.npz: scipy.fft analytic signals of long axes (2048: cfg5
+    and sta-paper n_z; 4096) -- outputs only, the inputs are rebuilt from
+    cases.long_lanes(n, lanes, dtype) (general N is checked against the
+    oracle, scipy itself, at test time)."""
+    out = {}
+    for n, l32, l64 in cases.LONG_AXES:
+        out[f"z32_{n}"] = ES.analytic_signal(cases.long_lanes(n, l32, np.float32), axis=0)
+        out[f"z64_{n}"] = ES.analytic_signal(cases.long_lanes(n, l64, np.float64), axis=0)
+    np.savez_compressed(os.path.join(HERE, "sigproc_long.npz"), **out)
+
+
+ALL = ("das_small", "chain", "sigproc", "fir", "qus", "formats", "sim", "configs", "engine",
+       "sigproc_long")
+
 if __name__ == "__main__":
-    for fn in (das_small, chain, sigproc, fir, qus, formats, sim, configs):
+    names = sys.argv[1:] or ALL
+    for fn in (globals()[n] for n in names):
         t = time.time()
         fn()
         print(fn.__name__, f"{time.time() - t:.1f}s", flush=True)

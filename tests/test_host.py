@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "bmode200.h")).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(bm_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(bm_\w+)\(", src, re.M)))
 
 
 def test_library_built_for_sm100a_and_exports_header_symbols():
@@ -33,7 +33,7 @@ def test_library_built_for_sm100a_and_exports_header_symbols():
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES), "ctypes signatures out of sync with the header"
     lib.bm_abi_version.restype = ctypes.c_int
-    assert lib.bm_abi_version() == 2
+    assert lib.bm_abi_version() == 3
     lib.bm_error_string.restype = ctypes.c_char_p
     assert lib.bm_error_string(4) == b"analytic signal needs axis length >= 2"
 
@@ -57,8 +57,26 @@ def test_invalid_arguments_rejected_without_gpu():
     lib = N.load()
     g = N.DasGeometry()
     assert lib.bm_das_beamform(ctypes.byref(g), None, 0, None, 0, 1, None) == 1
-    assert lib.bm_analytic_signal(0, None, None, 1, 8, 1, None) == 1
+    assert lib.bm_analytic_signal(0, None, None, 1, 8, 1, None, 0, None) == 1
+    assert lib.bm_envelope_display(0, None, None, None, None, 1, 8, 4, 30.0, None, 0, None) == 1
     assert lib.bm_display(0, None, None, None, None, 1, 4, 30.0, None) == 1
+    assert lib.bm_display_tiles(0, None, 2, 9, 2, 4, None, None, 30.0, None) == 1
+    assert lib.bm_pad_traces(0, None, 8, 1, 8, None, 8, None) == 1
+
+
+def test_debug_overrides_roundtrip_without_gpu():
+    """Tuning hooks are process-wide integers behind bm_debug_set/get (the
+    library reads no environment variables); the context manager restores
+    the previous value."""
+    lib = N.load()
+    assert lib.bm_debug_get(N.DEBUG_KEYS["das_ft"]) == 0
+    with N.debug_overrides(das_ft=2, fft_path=3):
+        assert lib.bm_debug_get(N.DEBUG_KEYS["das_ft"]) == 2
+        assert lib.bm_debug_get(N.DEBUG_KEYS["fft_path"]) == 3
+    assert lib.bm_debug_get(N.DEBUG_KEYS["das_ft"]) == 0
+    assert lib.bm_debug_get(99) == 0 and lib.bm_debug_set(-1, 5) == 0
+    src = "".join(open(p).read() for p in B.sources())
+    assert "getenv" not in src
 
 
 def test_no_cpu_fallback():
@@ -156,11 +174,10 @@ def test_no_contracted_fma_in_das_kernels():
     with a zero addend (a plain rounded product) and scalar FFMA only inside
     the correctly-rounded sqrt/div sequences."""
     funcs = _sass_by_function()
-    das = {n: l for n, l in funcs.items()
-           if any(k in n for k in ("das_fast_kernel", "das_tmem_kernel", "das_tma_kernel"))}
-    # (smem, tmem-scalar, tmem-pair, tmem-hybrid, tmem-pair-64ch, tma-32ch, tma-64ch,
-    # weighted tma-32ch, weighted tma-64ch) x {STA, PW} x {nearest, linear} x {t0, no t0}
-    # x {identity map, general} + 2 tma-128ch (uniform linear identity-map, STA | PW)
+    das = {n: l for n, l in funcs.items() if "das_tma_kernel" in n}
+    # (tma-32ch, tma-64ch, weighted tma-32ch, weighted tma-64ch) x {STA, PW}
+    # x {nearest, linear} x {t0, no t0} x {identity map, general}
+    # + 2 tma-128ch (uniform linear identity-map, STA | PW)
     # + 32 two-frames-per-pass tma (identity map) x {32, 64}ch x {uniform, weighted}
     # + 20 two-frames-per-thread tma (uniform identity map, no t0) x {STA, PW} x
     # {nearest, linear}: FP = 1 x {32, 64}ch, FP = 2 x {16, 32, 64}ch
@@ -169,19 +186,14 @@ def test_no_contracted_fma_in_das_kernels():
     # + 32 uniform four-frames-per-thread 16ch tma with a compile-time window
     #   (96 / 128 / 160 / 192 samples) x FP = 1 / 2 x {STA, PW} x {nearest, linear}
     # + 8 weighted FP = 2 ones with a 96-sample compile-time window, 16 / 32ch
-    assert len(das) == 270
+    assert len(das) == 190
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
                 assert "RZ" in l.split("FFMA2", 1)[1].split(";")[0], (n, l)
-        # floor via the magic constant, rounding toward -inf: packed (FADD2) for
-        # the pair kernels, scalar for the one-pixel-per-thread TMEM kernel
-        packed = not n.startswith("_ZN2bm15das_tmem_kernelILb0")
-        assert any(("FADD2.RM" if packed else "FADD.RM") in l for l in lines), n
-        if "das_tma_kernel" in n:  # TMA window staging, mbarrier pipeline
-            assert any("UTMALDG" in l for l in lines), n
-            assert any("SYNCS" in l for l in lines), n
-        else:
-            assert any("LDGSTS" in l for l in lines), n    # cp.async staging
-        if "das_tmem_kernel" in n or "das_tma_kernel" in n:  # delay table in tensor memory
-            assert any("LDTM" in l for l in lines) and any("STTM" in l for l in lines), n
+        # floor via the magic constant, rounding toward -inf, packed (FADD2)
+        assert any("FADD2.RM" in l for l in lines), n
+        # TMA window staging, mbarrier pipeline, delay table in tensor memory
+        assert any("UTMALDG" in l for l in lines), n
+        assert any("SYNCS" in l for l in lines), n
+        assert any("LDTM" in l for l in lines) and any("STTM" in l for l in lines), n

@@ -1,6 +1,7 @@
 """Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU logic:
-frame partitioning and the lateral column split of one large frame with the
-all-reduce(MAX) of the peak and the gather of display slabs.  Per-rank
+frame partitioning, the lateral column split of one large frame (one gather
+of [envelope | peak] tiles to the destination) and the depth-row split (one
+gather of RF bands).  Per-rank
 compute is the CPU oracle here (test infrastructure); on GPUs it is the
 bm_* kernels (tests/test_gpu_parallel.py checks that path on one device)."""
 
@@ -54,19 +55,31 @@ def _worker(rank, world, port, out_path):
         ctx, grid, rf = _geometry()
         split = P.LateralSplit(grid, world, rank)
         rf_slab = O.das_beamform(rf, ctx, split.sub_grid)                 # per-rank DAS
-        env = torch.from_numpy(np.abs(O.analytic_signal(rf_slab, axis=0)))  # rank-local lanes
-        rf_full = split.gather(torch.from_numpy(rf_slab))
-        disp = split.display(env, 30.0)
+        env = np.abs(O.analytic_signal(rf_slab, axis=0)).astype(np.float32)  # rank-local lanes
+        # the tile bm_envelope_peak fills on a GPU: envelope, then the peak bits
+        tile = split.send_tile(torch.float32, "cpu")
+        env_v, peak_v = split.tile_views(tile)
+        env_v.copy_(torch.from_numpy(env))
+        peak_v.copy_(torch.from_numpy(np.array([env.max()], np.float32).view(np.int32)))
+        recv = split.recv_tiles(torch.float32, "cpu") if rank == 0 else None
+        got = split.gather(tile, recv)                                    # THE collective
         if rank == 0:
-            np.savez(out_path, rf=rf_full.numpy(), disp=disp.numpy())
+            envs = [split.envelope_view(got[r], r).numpy() for r in range(world)]
+            peaks = got[:, -1].view(torch.int32).numpy().view(np.float32)
+            np.savez(out_path, env=np.concatenate(envs, axis=1), peaks=peaks,
+                     widths=np.array([e.shape[1] for e in envs]))
         else:
-            assert disp is None
+            assert got is None
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_lateral_split_gloo_matches_single_process(tmp_path, world):
+    """Column split of one frame (cfg5): every rank's [envelope | peak] tile
+    reaches dst in one gather, laid out as bm_display_tiles reads it; the
+    stitched envelope is the single-process one and the max of the tile peaks
+    is its peak, so dst's display is the single-process display."""
     from oracle import oracle as O
 
     out = str(tmp_path / "out.npz")
@@ -74,11 +87,13 @@ def test_lateral_split_gloo_matches_single_process(tmp_path, world):
     got = np.load(out)
     ctx, grid, rf = _geometry()
     rf_ref, env_ref, disp_ref = O.bmode_chain(rf, ctx, grid)
-    # DAS is per pixel: the stitched slabs are bitwise the single-process image
-    assert got["rf"].tobytes() == rf_ref.tobytes()
-    # display against the all-reduced global peak
-    assert np.abs(got["disp"] - disp_ref).max() <= 1e-6
-    assert got["disp"].max() == 1.0
+    assert [h - l for l, h in P.column_slabs(grid.n_x, world)] == list(got["widths"])
+    assert np.abs(got["env"] - env_ref).max() <= 1e-6 * env_ref.max()
+    assert got["peaks"].max() == got["env"].max()
+    # the mapping bm_display_tiles applies, with the gathered global peak
+    disp = O.dynamic_adjustment_with_peak(got["env"], got["peaks"].max(), 30.0)
+    assert np.abs(disp - disp_ref).max() <= 1e-5
+    assert disp.max() == 1.0
 
 
 def _row_worker(rank, world, port, out_path):
@@ -89,8 +104,11 @@ def _row_worker(rank, world, port, out_path):
     try:
         ctx, grid, rf = _geometry()
         split = P.RowSplit(grid, world, rank)
+        send = split.send_band(torch.float32, "cpu")
         band = O.das_beamform(rf, ctx, split.sub_grid)          # per-rank DAS of a depth band
-        rf_full = split.gather(torch.from_numpy(band))          # the only collective
+        send[: band.shape[0]] = torch.from_numpy(band)
+        recv = split.recv_bands(torch.float32, "cpu") if rank == 0 else None
+        rf_full = split.gather(send, recv)                      # the only collective
         if rank == 0:
             np.savez(out_path, rf=rf_full.numpy())
         else:
