@@ -111,6 +111,9 @@ typedef struct bm_das_geometry {
                                 contiguous maps, log2 of the lane-block width:
                                 3 = 16 x 16 pixels (lane blocks 4 x 8), 2 = 32 x 8,
                                 1 = 64 x 4, 4 = 8 x 32; window_hint_g4 is for it */
+  const float* rx_table;     /* optional DEVICE table from bm_das_build_table: the
+                                receive delays of every tile, read instead of being
+                                rebuilt by each CTA (same bits); NULL = rebuild */
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64
@@ -141,6 +144,17 @@ int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride);
  * -1 when another kernel would run.  Host only. */
 int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_stride, int32_t n_frames,
                         int32_t* shape);
+
+/* Per-plan receive-delay table of the TMA kernel (the role of DasPlan's
+ * d_rx LUT, beamform.py:211-216, in the kernel's tile order): bytes, and the
+ * build (stream-ordered, one launch).  A launch with g->rx_table set reads
+ * each CTA's 128 pixel pairs x n_elements delays from it instead of
+ * evaluating fs*(sqrt(dx^2+z^2)/c) per CTA -- the dominant per-CTA cost of a
+ * one-frame launch.  Valid for the geometry (positions, c, fs, tile shape)
+ * it was built from.  0 / BM_ERR_UNSUPPORTED when the TMA kernel does not
+ * apply. */
+int64_t bm_das_table_bytes(const bm_das_geometry* g);
+int bm_das_build_table(const bm_das_geometry* g, float* table, void* stream);
 
 /* Delay-and-Sum of n_frames frames.
  *   rf : device dtype[n_frames][n_tx][n_rx][n_samples], frame f at rf + f*rf_frame_stride

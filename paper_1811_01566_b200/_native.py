@@ -47,6 +47,7 @@ class DasGeometry(ctypes.Structure):
         ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),
         ("rx_map", ctypes.c_void_p), ("t0_smp", ctypes.c_void_p), ("hann", ctypes.c_void_p),
         ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32), ("tile_ls", ctypes.c_int32),
+        ("rx_table", ctypes.c_void_p),
     ]
 
 
@@ -57,6 +58,8 @@ SIGNATURES = {
     "bm_das_prepare": ([ctypes.POINTER(DasGeometry), _P, _P, _P, _P, _P], ctypes.c_int),
     "bm_das_select": ([ctypes.POINTER(DasGeometry), _I64], ctypes.c_int),
     "bm_das_launch_shape": ([ctypes.POINTER(DasGeometry), _I64, _I32, _P], ctypes.c_int),
+    "bm_das_table_bytes": ([ctypes.POINTER(DasGeometry)], _I64),
+    "bm_das_build_table": ([ctypes.POINTER(DasGeometry), _P, _P], ctypes.c_int),
     "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
     "bm_sigproc_ws_bytes": ([_I32, _I32, _I64, _I64, _I64], _I64),
     "bm_pad_traces": ([_I32, _P, _I64, _I64, _I64, _P, _I64, _P], ctypes.c_int),

@@ -26,6 +26,7 @@
 // Several frames per pass (FP warp groups x FT frames per thread) share the
 // table and the frame-independent work; see the kernel's comment.
 #include <cuda.h>  // CUtensorMap
+#include <algorithm>
 #include <stdio.h>
 
 #include "bm_tmem.cuh"
@@ -100,6 +101,47 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+
+// exact receive delays fs*(sqrt(dx*dx + z*z)/c) of element m for a pixel
+// pair at (px, pzA) / (px, pzB), dx = T(elem_x - px) (beamform.py:211-216)
+__device__ __forceinline__ float2 rx_delay_pair(const bm_das_geometry& g, int m, double px,
+                                                float pzA, float pzB, float c, float fs) {
+  using O = R<float>;
+  const float dx = O::from_double(g.elem_x[m] - px);
+  const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
+  const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
+  return make_float2(dA, dB);
+}
+
+// Pixel pair of consumer thread ctid (0..127) of a tile: the mapping of
+// das_tma_kernel (warp w & 3 picks the 2 x 2 warp block, lane the pair).
+struct PairPos {
+  int col, rowA, rowB;
+  __device__ PairPos(const bm_das_geometry& g, int ls, int tile, int ctid) {
+    const int CA = 1 << ls, RA = 32 >> ls, TZk = 4 * RA, TXk = 2 * CA;
+    const int tiles_x = (g.n_x + TXk - 1) / TXk, warp = ctid >> 5, lane = ctid & 31;
+    const int tz0 = (tile / tiles_x) * TZk, tx0 = (tile % tiles_x) * TXk;
+    col = tx0 + (warp & 1) * CA + (lane & (CA - 1));
+    rowA = tz0 + ((warp >> 1) & 1) * 2 * RA + (lane >> ls);
+    rowB = rowA + RA;
+  }
+};
+
+// bm_das_build_table: table[tile][m][ctid] = delays of the thread's pair
+__global__ void __launch_bounds__(128) das_table_kernel(const bm_das_geometry g, int ls,
+                                                        float2* __restrict__ table) {
+  using O = R<float>;
+  const PairPos pp(g, ls, blockIdx.x, threadIdx.x);
+  const int colc = min(pp.col, g.n_x - 1);
+  const int rAc = min(pp.rowA, g.n_z - 1), rBc = min(pp.rowB, g.n_z - 1);
+  const float c = O::from_double(g.speed_of_sound);
+  const float fs = O::from_double(g.sampling_frequency);
+  const double px = g.x_pos[colc];
+  const float pzA = O::from_double(g.z_pos[rAc]), pzB = O::from_double(g.z_pos[rBc]);
+  float2* tb = table + (int64_t)blockIdx.x * g.n_elements * 128 + threadIdx.x;
+  for (int m = blockIdx.y; m < g.n_elements; m += gridDim.y)
+    tb[(int64_t)m * 128] = rx_delay_pair(g, m, px, pzA, pzB, c, fs);
 }
 
 // WT: non-uniform receive apodisation (Hann and/or F-number gate): the
@@ -211,12 +253,29 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   int wlo = 0, whi = n_el - 1;
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
   if (!producer) {
-    // the FP warps sharing a lane quarter split the elements
-    for (int m = slot; m < n_el; m += FP) {
-      const float dx = O::from_double(g.elem_x[m] - px);
-      const float dA = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzA, pzA))), c));
-      const float dB = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pzB, pzB))), c));
-      tm_st2(tlane + 2 * m, dA, dB);
+    if (g.rx_table) {
+      // precomputed per plan (bm_das_build_table, the same bits): 8 loads in
+      // flight per thread, streamed past L2 (the RF windows want it)
+      const float2* tb =
+          reinterpret_cast<const float2*>(g.rx_table) + (int64_t)blockIdx.x * n_el * NC + ctid;
+      int m = slot;
+      for (; m + 7 * FP < n_el; m += 8 * FP) {
+        float2 d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[u] = __ldcs(tb + (int64_t)(m + u * FP) * NC);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tm_st2(tlane + 2 * (m + u * FP), d[u].x, d[u].y);
+      }
+      for (; m < n_el; m += FP) {
+        const float2 d = __ldcs(tb + (int64_t)m * NC);
+        tm_st2(tlane + 2 * m, d.x, d.y);
+      }
+    } else {
+      // the FP warps sharing a lane quarter split the elements
+      for (int m = slot; m < n_el; m += FP) {
+        const float2 d = rx_delay_pair(g, m, px, pzA, pzB, c, fs);
+        tm_st2(tlane + 2 * m, d.x, d.y);
+      }
     }
     if (WT) {
       // receive apodisation (beamform.py:84-109): weight of element m is
@@ -855,3 +914,17 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
 }
 
 }  // namespace bm
+
+extern "C" int64_t bm_das_table_bytes(const bm_das_geometry* g) {
+  if (!g || g->dtype != BM_F32 || g->n_elements < 1 || g->n_z < 1 || g->n_x < 1) return 0;
+  return (int64_t)bm::tma_tiles(*g) * g->n_elements * 128 * 8;
+}
+
+extern "C" int bm_das_build_table(const bm_das_geometry* g, float* table, void* stream) {
+  if (!g || !table || !g->elem_x || !g->x_pos || !g->z_pos) return BM_ERR_INVALID_ARGUMENT;
+  if (bm_das_table_bytes(g) <= 0) return BM_ERR_UNSUPPORTED;
+  const dim3 grid((unsigned)bm::tma_tiles(*g), (unsigned)std::min(g->n_elements, 16));
+  bm::das_table_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*g, bm::tma_ls(*g),
+                                                               reinterpret_cast<float2*>(table));
+  return bm::cuda_status();
+}

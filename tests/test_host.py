@@ -50,7 +50,8 @@ def test_geometry_struct_layout():
     # compiler lays out bm_das_geometry
     assert N.DasGeometry.rx_contig.offset == 16 * 4 + 2 * 8 + 10 * 8
     assert N.DasGeometry.tile_ls.offset == 16 * 4 + 2 * 8 + 10 * 8 + 4
-    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 8
+    assert N.DasGeometry.rx_table.offset == 16 * 4 + 2 * 8 + 10 * 8 + 8
+    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 8 + 8
 
 
 def test_invalid_arguments_rejected_without_gpu():
