@@ -254,17 +254,18 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
   if (!producer) {
     if (g.rx_table) {
-      // precomputed per plan (bm_das_build_table, the same bits): 8 loads in
-      // flight per thread, streamed past L2 (the RF windows want it)
+      // precomputed per plan (bm_das_build_table, the same bits): 32 loads
+      // in flight per thread (a CTA's 128 KB arrives at ~HBM latency x 4, not
+      // x 16), streamed past L2 (the RF windows want it)
       const float2* tb =
           reinterpret_cast<const float2*>(g.rx_table) + (int64_t)blockIdx.x * n_el * NC + ctid;
       int m = slot;
-      for (; m + 7 * FP < n_el; m += 8 * FP) {
-        float2 d[8];
+      for (; m + 31 * FP < n_el; m += 32 * FP) {
+        float2 d[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) d[u] = __ldcs(tb + (int64_t)(m + u * FP) * NC);
+        for (int u = 0; u < 32; ++u) d[u] = __ldcs(tb + (int64_t)(m + u * FP) * NC);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tm_st2(tlane + 2 * (m + u * FP), d[u].x, d[u].y);
+        for (int u = 0; u < 32; ++u) tm_st2(tlane + 2 * (m + u * FP), d[u].x, d[u].y);
       }
       for (; m < n_el; m += FP) {
         const float2 d = __ldcs(tb + (int64_t)m * NC);
@@ -678,7 +679,12 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
   const int only = debug_override(BM_DBG_DAS_TJC);  // tuning override: 32 | 64 | 128
   for (int t : {128, 64, 32, 16}) {
     if (t > g.n_rx && t > 32) continue;
-    if (t == 128 && (!tma_has128(g) || fp != 1)) continue;
+    // 128-channel stages (one-frame launches: the only ones with fp == 1
+    // left): one stage boundary per 128 channels pays on launches of many
+    // waves (cfg3 / cfg5: 3.13 -> 3.08 / 24.3 -> 23.6 ms); a few-wave launch
+    // fills its pipeline sooner with 64 x 4 stages (cfg2 0.174 -> 0.168 ms)
+    if (t == 128 && (!tma_has128(g) || fp != 1 || (only != 128 && tma_tiles(g) < 1800)))
+      continue;
     if (t == 16 && fp < 4) continue;  // 16-channel stages: four frames per pass only
     if (t > max_t) continue;          // no kernel instantiated for this stage size
     if (only && t != only) continue;

@@ -12,7 +12,13 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_1811_01566_b200 as bm  # noqa: E402
 
-only = sys.argv[1:] or ["cfg2", "cfg1", "cfg3", "cfg5", "sta-paper", "pwi-paper"]
+from paper_1811_01566_b200 import _native as N  # noqa: E402
+
+args = [a for a in sys.argv[1:] if "=" not in a]
+for kv in (a for a in sys.argv[1:] if "=" in a):  # library tuning hooks, e.g. das_tjc=64
+    k, v = kv.split("=")
+    N.load().bm_debug_set(N.DEBUG_KEYS[k], int(v))
+only = args or ["cfg2", "cfg1", "cfg3", "cfg5", "sta-paper", "pwi-paper"]
 res = {}
 for name in only:
     ctx, grid, n_s = bm.environment.config_geometry(name)

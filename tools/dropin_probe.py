@@ -49,3 +49,23 @@ print("execute (no readback) ms", t(ex))
 print("execute + numpy ms", t(lambda: ex()["dynamic_adjustment"].numpy()))
 outs, tm = bm.execute(g, (frames[0], ctx))
 print("stages", tm.stages, "total", tm.total_ms)
+
+from paper_1811_01566_b200 import _device as D  # noqa: E402
+
+print("staged to_device ms", t(lambda: D.to_device(host[0], dev)))
+for step_div in (1, 2, 4, 8):
+    def staged(div=step_div):
+        src = torch.from_numpy(host[0]).reshape(-1)
+        n = src.numel()
+        step = -(-n // div)
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+        for o in range(0, n, step):
+            pin[:].view(-1)[o:o + step].copy_(src[o:o + step])
+            out[o:o + step].copy_(pin.view(-1)[o:o + step], non_blocking=True)
+        return out
+    print("manual staged chunks", step_div, "ms", t(staged))
+img_h = np.empty(grid.shape, np.float32)
+dd = torch.empty(grid.shape, device=dev)
+print("d2h 1 MB .cpu() ms", t(lambda: dd.cpu()))
+r1 = bm.RfFrame(host[0])
+print("das_beamform drop-in (numpy in, numpy out) ms", t(lambda: bm.das_beamform(r1, ctx, grid, plan=plan)))
