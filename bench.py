@@ -285,13 +285,20 @@ def das_roofline(eng, ctx, grid, n_s, B, das_ms, interp, clk, n_sm, peaks, workl
     n_rx = ctx.rx_channel_map.shape[1] if ctx.rx_channel_map is not None else ctx.n_elements
     contrib = B * ctx.n_tx * n_rx * grid.n_z * grid.n_x
     span = eng.plan._bufs.get("span")
-    if span is not None and eng.plan._geom.rx_identity:
+    if span is not None and eng.plan._geom.rx_contig:
         # F-number gate: terms outside a pixel's active span have weight 0 and
         # are exact zeros the kernel skips -- the algorithmic work is the
-        # active contributions
+        # active contributions: per transmit, the span clipped to the run of
+        # elements that transmit records (identity or centred maps)
         sp = span.view(-1, 2).to(torch.int64)
-        lo, hi = sp[:, 0].clamp(min=0), sp[:, 1].clamp(max=ctx.n_elements - 1)
-        contrib = int(B * ctx.n_tx * (hi - lo + 1).clamp(min=0).sum().item())
+        rmap = ctx.channel_elements(n_rx)
+        active = 0
+        for e in range(ctx.n_tx):
+            first = int(rmap[e][0])
+            lo = sp[:, 0].clamp(min=first)
+            hi = sp[:, 1].clamp(max=first + n_rx - 1)
+            active += int((hi - lo + 1).clamp(min=0).sum().item())
+        contrib = B * active
     sm_mhz = clk.get("sm_mhz") or 1965.0
     shape = eng.plan.launch_shape(n_s, B, interp) or {"ft": 1, "fp": 1}
     ft = shape["ft"]

@@ -22,11 +22,12 @@
 // owns pixels A (row l >> ls, col l & (2^ls - 1) of its block) and B (A +
 // 32 >> ls rows), ls = 3 giving 16 x 16 tiles of 8 x 8 blocks (tile_ls picks
 // 32 x 8, 64 x 4 or 8 x 32 for other grids).  TMEM lane 32 (w & 3) + l holds
-// the pair's delays to element m in columns 2m, 2m+1 (weights after them).
+// the pair's delays to element m in columns 2m, 2m+1.
 // Several frames per pass (FP warp groups x FT frames per thread) share the
 // table and the frame-independent work; see the kernel's comment.
 #include <cuda.h>  // CUtensorMap
 #include <algorithm>
+#include <type_traits>
 #include <stdio.h>
 
 #include "bm_tmem.cuh"
@@ -144,10 +145,14 @@ __global__ void __launch_bounds__(128) das_table_kernel(const bm_das_geometry g,
     tb[(int64_t)m * 128] = rx_delay_pair(g, m, px, pzA, pzB, c, fs);
 }
 
-// WT: non-uniform receive apodisation (Hann and/or F-number gate): the
-// per-pixel weights w[m] live in TMEM next to the delays (columns
-// 2*n_el + 2m, 2m+1), and a contribution is acc + (w*(1-a))*x0 + (w*a)*x1
-// exactly as beamform.py:175-187 rounds it.
+// WT: non-uniform receive apodisation (Hann and/or F-number gate): a
+// contribution is acc + (w*(1-a))*x0 + (w*a)*x1 exactly as beamform.py:175-187
+// rounds it, with the weight w[m] of each pixel formed in registers per
+// 4-channel group -- the Hann element row (no F-number: the same row for
+// every pixel), 1 / 0 from the pixel's active span (rectangular +
+// F-number), or the span's Hann row, both rows read through L1 -- so the
+// delay table alone fills TMEM (2 columns per element) and two CTAs share an
+// SM.
 //
 // FP = 2: two frames per pass.  Consumer warps w and w + 4 own the same pixel
 // pairs (the same TMEM lane quarter, so they share one delay table) but
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(128) das_table_kernel(const bm_das_geometry g,
 // {W, G, FP * FT}); each accumulator keeps the reference's e -> j order.
 template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false, int FP = 1,
           int FT = 1, int WI = 0>
-__global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
+__global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
     das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
   using O = R<float>;
   using L = Lane<true>;
@@ -231,9 +236,9 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     tm_alloc(smem_s, (uint32_t)a.tmem_cols);
     tm_relinquish();
   }
-  if (SKIP && tid == 0) {
-    espan[0] = n_el;
-    espan[1] = -1;
+  if (SKIP && tid == 0) {  // without an F-number every element is active
+    espan[0] = g.span ? n_el : 0;
+    espan[1] = g.span ? -1 : n_el - 1;
   }
   if (producer && lane == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -251,6 +256,8 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
 
   // SKIP: union of the active spans of this warp's 64 pixels (warp-uniform)
   int wlo = 0, whi = n_el - 1;
+  // WT: the pair's active element spans (all elements without an F-number)
+  int i0A = 0, i1A = n_el - 1, i0B = 0, i1B = n_el - 1;
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
   if (!producer) {
     if (g.rx_table) {
@@ -278,41 +285,28 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
         tm_st2(tlane + 2 * m, d.x, d.y);
       }
     }
-    if (WT) {
+    if (WT && g.span) {
       // receive apodisation (beamform.py:84-109): weight of element m is
       // window[m - i0] inside the pixel's active span [i0, i1], 0 outside
-      int i0A = 0, i1A = n_el - 1, i0B = 0, i1B = n_el - 1;
-      if (g.span) {
-        const int64_t pA = (int64_t)rAc * g.n_x + colc, pB = (int64_t)rBc * g.n_x + colc;
-        i0A = g.span[2 * pA];
-        i1A = g.span[2 * pA + 1];
-        i0B = g.span[2 * pB];
-        i1B = g.span[2 * pB + 1];
-      }
-      auto row = [&](int i0, int i1) -> const float* {
-        if (g.window != BM_HANN) return nullptr;
-        const int cnt = max(0, min(i1 - i0 + 1, n_el));
-        return reinterpret_cast<const float*>(g.hann) + (int64_t)cnt * n_el;
-      };
-      const float* hA = row(i0A, i1A);
-      const float* hB = row(i0B, i1B);
-      if (SKIP) {
-        int lo = n_el, hi = -1;
-        if (i0A <= i1A) lo = min(lo, i0A), hi = max(hi, i1A);
-        if (i0B <= i1B) lo = min(lo, i0B), hi = max(hi, i1B);
-        lo = max(lo, 0);
-        hi = min(hi, n_el - 1);
-        if (slot == 0 && hi >= 0) {
+      const int64_t pA = (int64_t)rAc * g.n_x + colc, pB = (int64_t)rBc * g.n_x + colc;
+      i0A = g.span[2 * pA];
+      i1A = g.span[2 * pA + 1];
+      i0B = g.span[2 * pB];
+      i1B = g.span[2 * pB + 1];
+      int lo = n_el, hi = -1;
+      if (i0A <= i1A) lo = min(lo, i0A), hi = max(hi, i1A);
+      if (i0B <= i1B) lo = min(lo, i0B), hi = max(hi, i1B);
+      lo = max(lo, 0);
+      hi = min(hi, n_el - 1);
+      if (slot == 0 && hi >= 0) {
+        if (SKIP) {
           atomicMin(&espan[0], lo);
           atomicMax(&espan[1], hi);
         }
+      }
+      if (SKIP) {
         wlo = __reduce_min_sync(0xffffffffu, lo);
         whi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi + 1)) - 1;
-      }
-      for (int m = slot; m < n_el; m += FP) {
-        const float wA = (m >= i0A && m <= i1A) ? (hA ? hA[m - i0A] : 1.0f) : 0.0f;
-        const float wB = (m >= i0B && m <= i1B) ? (hB ? hB[m - i0B] : 1.0f) : 0.0f;
-        tm_st2(tlane + 2 * n_el + 2 * m, wA, wB);
       }
     }
     tm_wait_st();
@@ -361,6 +355,27 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
     }
   }
   __syncthreads();
+
+  // WT: the Hann rows (beamform.py:48-63) are read through L1 from the
+  // plan's table: the element row without an F-number (one row for every
+  // pixel), else the row of each pixel's span width -- a tile's pixels use a
+  // handful of rows, so they stay L1-resident
+  const float* hglob = reinterpret_cast<const float*>(g.hann);
+  const bool hann = WT && g.window == BM_HANN;
+  auto hann_row = [&](int i0, int i1) -> const float* {
+    const int cnt = g.span ? max(0, min(i1 - i0 + 1, n_el)) : n_el;
+    return hglob + (int64_t)cnt * n_el;
+  };
+  const float* hrA = hann ? hann_row(i0A, i1A) : nullptr;
+  const float* hrB = hann ? hann_row(i0B, i1B) : nullptr;
+  // receive weights (w_A, w_B) of element m (beamform.py:84-109)
+  auto weight_pair = [&](int m) -> u64 {
+    if (hann && !g.span) return L::splat(__ldg(hrA + m));
+    const bool inA = m >= i0A && m <= i1A, inB = m >= i0B && m <= i1B;
+    const float wA = inA ? (hann ? __ldg(hrA + (m - i0A)) : 1.0f) : 0.0f;
+    const float wB = inB ? (hann ? __ldg(hrB + (m - i0B)) : 1.0f) : 0.0f;
+    return L::make(wA, wB);
+  };
 
   const int n_chunks = (n_rx + TJC - 1) / TJC;
   const int f_begin = blockIdx.y * a.frames_per_cta;
@@ -536,15 +551,22 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
       if (IDMAP && jn == TJC) {
         // identity map: channel j is element j -- one tcgen05.ld.x32 fetches
         // the delay pairs of 16 consecutive channels
-        auto group = [&](const uint32_t(&r)[32], const uint32_t(&w)[32], int h) {
+        // m0: element of the group's first channel (weights formed 4 at a time)
+        auto group = [&](const uint32_t(&r)[32], int m0, int h, auto check) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4) {
+            // SKIP: 4 channels outside every pixel's aperture of this warp are
+            // exact zeros (warp-uniform; tested only on groups that straddle
+            // the aperture's edge, so the common case keeps one schedule)
+            if (decltype(check)::value && (m0 + i > whi || m0 + i + 3 < wlo)) continue;
             const int4 k4 = MK4[(h + i) >> 2];
 #define BM_PAIR(R, q) (((u64)R[2 * (i + q) + 1] << 32) | R[2 * (i + q)])
-            channel(BM_PAIR(r, 0), WT ? BM_PAIR(w, 0) : 0ull, (uint32_t)k4.x);
-            channel(BM_PAIR(r, 1), WT ? BM_PAIR(w, 1) : 0ull, (uint32_t)k4.y);
-            channel(BM_PAIR(r, 2), WT ? BM_PAIR(w, 2) : 0ull, (uint32_t)k4.z);
-            channel(BM_PAIR(r, 3), WT ? BM_PAIR(w, 3) : 0ull, (uint32_t)k4.w);
+#define BM_W(q) (WT ? weight_pair(m0 + i + q) : 0ull)
+            channel(BM_PAIR(r, 0), BM_W(0), (uint32_t)k4.x);
+            channel(BM_PAIR(r, 1), BM_W(1), (uint32_t)k4.y);
+            channel(BM_PAIR(r, 2), BM_W(2), (uint32_t)k4.z);
+            channel(BM_PAIR(r, 3), BM_W(3), (uint32_t)k4.w);
+#undef BM_W
 #undef BM_PAIR
           }
         };
@@ -555,21 +577,19 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), (FP == 2 && WT) ? 1 : 2)
             const int m0 = rxb[cur.e] + cur.cb * TJC + h;
             if (m0 > whi || m0 + 15 < wlo) continue;
           }
-          uint32_t r[32], w[32];
+          uint32_t r[32];
           tm_ld32_issue(tc + 2 * h, r);
-          if (WT) {
-            tm_ld32_issue(tc + 2 * n_el + 2 * h, w);
-            tm_wait_regs2(r, w);
-          } else {
-            tm_wait_regs(r);
-          }
-          group(r, w, h);
+          tm_wait_regs(r);
+          const int m0 = rxb[cur.e] + cur.cb * TJC + h;
+          if (SKIP && (m0 < wlo || m0 + 15 > whi))
+            group(r, m0, h, std::true_type{});
+          else
+            group(r, m0, h, std::false_type{});
         }
       } else {
         for (int jj = 0; jj < jn; ++jj) {
           const int m = IDMAP ? rxb[cur.e] + cur.cb * TJC + jj : MMc[jj];
-          channel((VT)tm_ld2(tlane + 2 * m), WT ? (VT)tm_ld2(tlane + 2 * n_el + 2 * m) : 0ull,
-                  (uint32_t)MKc[jj]);
+          channel((VT)tm_ld2(tlane + 2 * m), WT ? (VT)weight_pair(m) : 0ull, (uint32_t)MKc[jj]);
         }
       }
       // every gathered sample feeds acc: pinning acc before the arrive keeps
@@ -657,7 +677,7 @@ static int tma_tiles(const bm_das_geometry& g) {
 // TMEM columns of one CTA: delay pairs (2 per element) plus, with
 // non-uniform apodisation, weight pairs (2 more per element)
 static int tma_cols(const bm_das_geometry& g) {
-  const int need = (g.uniform ? 2 : 4) * g.n_elements;
+  const int need = 2 * g.n_elements;
   return need <= 256 ? 256 : 512;
 }
 
@@ -689,7 +709,9 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
     if (t > max_t) continue;          // no kernel instantiated for this stage size
     if (only && t != only) continue;
     int n = kTmaMaxStages;
-    while (n >= 2 && (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw, fp).total > cap) --n;
+    while (n >= 2 &&
+           (size_t)TmaLayout(g.n_tx, g.n_elements, t, n, W, pw, fp).total > cap)
+      --n;
     if (n >= (t == 64 && fp == 1 ? 3 : 2)) {
       tjc = t;
       nst = n;
@@ -702,7 +724,7 @@ static bool tma_plan(const bm_das_geometry& g, int fp, int& tjc, int& nst, size_
 
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride) {
   if (g.dtype != BM_F32 || g.window_hint <= 0 || tma_window(g) > 256) return 0;
-  if (!g.uniform && (4 * g.n_elements > 512 || (g.window == BM_HANN && !g.hann))) return 0;
+  if (!g.uniform && g.window == BM_HANN && !g.hann) return 0;
   if (g.rx_contig && g.window_hint_g4 <= 0) return 0;  // 4-channel boxes need the bound
   if (g.n_samples % 4 != 0 || rf_stride % 4 != 0) return 0;  // 16-B TMA strides
   if (2 * g.n_elements > 512) return 0;                       // pair layout in TMEM
