@@ -230,6 +230,10 @@ int bm_display_tiles(int32_t dtype, const void* tiles, int32_t n_tiles, int64_t 
                      int64_t n_z, int64_t n_x, void* disp, int32_t* status, double range_db,
                      void* stream);
 
+/* Finiteness scan of a device frame (RfFrame validation, types.py:41-42):
+ * *flag (device int32) = 1 if any value is NaN or +-inf, else 0. */
+int bm_check_finite(int32_t dtype, const void* x, int64_t count, int32_t* flag, void* stream);
+
 /* dynamic_adjustment as one call: bm_frame_peak then bm_display. */
 int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
                           int32_t* status, int32_t n_frames, int64_t frame_elems,

@@ -1153,6 +1153,34 @@ extern "C" int bm_display_tiles(int32_t dtype, const void* tiles, int32_t n_tile
   return cuda_status();
 }
 
+namespace bm {
+template <typename T>
+__global__ void nonfinite_kernel(const T* __restrict__ x, int64_t n, int32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+}  // namespace bm
+
+// RfFrame's finiteness scan (types.py:41-42) for device-resident frames:
+// *flag = 1 if any of the `count` values is NaN or infinite, else 0.
+extern "C" int bm_check_finite(int32_t dtype, const void* x, int64_t count, int32_t* flag,
+                               void* stream) {
+  if (!x || !flag || count < 0) return BM_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(flag, 0, sizeof(int32_t), s) != cudaSuccess) return BM_ERR_CUDA;
+  if (count == 0) return BM_OK;
+  if (dtype == BM_F32)
+    nonfinite_kernel<float><<<grid_for(count), 256, 0, s>>>((const float*)x, count, flag);
+  else if (dtype == BM_F64)
+    nonfinite_kernel<double><<<grid_for(count), 256, 0, s>>>((const double*)x, count, flag);
+  else
+    return BM_ERR_INVALID_ARGUMENT;
+  return cuda_status();
+}
+
 extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
                              int64_t frame_elems, void* stream) {
   if (!e || !peak || n_frames < 1 || n_frames > 65535 || frame_elems < 0)

@@ -63,7 +63,8 @@ class BmodeEngine:
             rf_img = torch.empty((n_frames, nz, nx), dtype=self.tdtype, device=self.device)
             peak = torch.empty(n_frames, dtype=torch.int32 if self.code == N.BM_F32 else torch.int64,
                                device=self.device)
-            status = torch.zeros(n_frames, dtype=torch.int32, device=self.device)
+            # written for every frame by the display kernels (no fill launch)
+            status = torch.empty(n_frames, dtype=torch.int32, device=self.device)
             with torch.cuda.device(self.device):
                 nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_DISPLAY, self.code, n_frames,
                                                       nz, nx))
@@ -103,7 +104,8 @@ class BmodeEngine:
         """Raise AllZeroInput if any frame of the last batch had no positive
         envelope sample (synchronises)."""
         st = getattr(self, "_last_status", None)
-        if st is not None and int(st.max().item()) != 0:
+        # a device->host copy of the per-frame words (no reduction kernel)
+        if st is not None and st.numel() and int(st.cpu().numpy().max()) != 0:
             raise AllZeroInput("dynamic adjustment needs a strictly positive element")
 
     # -------------------------------------------------------------------- host
@@ -172,7 +174,7 @@ class BmodeEngine:
 
         for b, (rf_host, disp_host) in enumerate(batches_all()):
             f = int(rf_host.shape[0])
-            status = torch.zeros(f, dtype=torch.int32, device=self.device)
+            status = torch.empty(f, dtype=torch.int32, device=self.device)
             statuses.append(status)
             for lo in range(0, f, chunk):
                 hi = min(f, lo + chunk)

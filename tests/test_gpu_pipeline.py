@@ -119,3 +119,21 @@ def test_staged_host_to_device_copies_are_exact_and_do_not_alias():
     assert torch.equal(small.cpu(), torch.from_numpy(hosts[0][:1, :1].copy()))
     f64 = to_device(hosts[1].astype(np.float64), dev)
     assert f64.dtype == torch.float64 and torch.equal(f64.cpu(), torch.from_numpy(hosts[1].astype(np.float64)))
+
+
+def test_device_frame_finiteness_scan_on_the_gpu():
+    """RfFrame of a CUDA tensor runs the reference's finiteness check
+    (types.py:41-42) with bm_check_finite: NaN and inf rejected."""
+    import torch
+
+    from paper_1811_01566_b200.errors import InvalidMetadata
+
+    x = torch.randn(3, 4, 257, device="cuda")
+    bm.RfFrame(x)
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        y = x.clone()
+        y[2, 3, 256] = bad
+        with pytest.raises(InvalidMetadata):
+            bm.RfFrame(y)
+        with pytest.raises(InvalidMetadata):
+            bm.RfFrame(y.double())
