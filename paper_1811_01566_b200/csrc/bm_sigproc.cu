@@ -705,7 +705,7 @@ static size_t lane_smem(const FftPlan& p, int L, int lstride) {
 }
 
 static int sig_plan(int32_t dtype, int64_t n, int64_t outer, int64_t inner, SigPlan* sp) {
-  if (n > 0x7fffffffLL / 2 || outer < 1 || inner < 1) return BM_ERR_UNSUPPORTED;
+  if (n > (1LL << 29) || outer < 1 || inner < 1) return BM_ERR_UNSUPPORTED;
   *sp = SigPlan{};
   sp->p = make_plan(n);
   if (dtype == BM_F32 && (n == 256 || n == 512 || n == 1024) && debug_override(BM_DBG_FFT_PATH) <= 0) {
