@@ -178,6 +178,15 @@ int64_t bm_sigproc_ws_bytes(int32_t op, int32_t dtype, int64_t outer, int64_t n,
 int bm_pad_traces(int32_t dtype, const void* src, int64_t src_pitch, int64_t n_traces,
                   int64_t n_samples, void* dst, int64_t dst_samples, void* stream);
 
+/* bm_das_beamform over the transmits [e_begin, e_end) only; with accumulate
+ * the per-pixel sums continue from the values already in `out` (same f32
+ * sums, same e -> j order, so consecutive ranges give bm_das_beamform's bits).
+ * Lets a caller start beamforming the first transmits of a frame while the
+ * host->device copy of the rest is still in flight. */
+int bm_das_beamform_range(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
+                          void* out, int64_t out_frame_stride, int32_t n_frames, int32_t e_begin,
+                          int32_t e_end, int32_t accumulate, void* stream);
+
 /* Analytic signal along the middle axis of a contiguous [outer, n, inner]
  * real array x; z is complex interleaved (re, im) of the same dtype.  Any
  * n >= 2 (mixed radix, Bluestein for prime factors > 61): ws / ws_bytes as

@@ -54,6 +54,41 @@ def _staged_h2d(src, device):
     return out
 
 
+def staged_copy_into(src, dst, stream):
+    """Copy a contiguous CPU tensor into the device tensor ``dst`` (same
+    numel) through the per-thread pinned staging buffers, enqueued on
+    ``stream``; returns the event that follows the last DMA."""
+    import torch
+
+    pool = getattr(_stage, "pool", None)
+    if pool is None:
+        pool = _stage.pool = {"bufs": [None, None], "events": [None, None], "next": 0}
+    i = pool["next"]
+    pool["next"] ^= 1
+    nbytes = src.numel() * src.element_size()
+    buf = pool["bufs"][i]
+    if buf is None or buf.numel() < nbytes:
+        buf = pool["bufs"][i] = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),
+                                            dtype=torch.uint8, pin_memory=True)
+        pool["events"][i] = None
+    ev = pool["events"][i]
+    if ev is not None:
+        ev.synchronize()  # the DMA that last read this buffer has finished
+    stage = buf[:nbytes].view(src.dtype)
+    flat, oflat = src.reshape(-1), dst.view(-1)
+    # in pieces: the DMA of one overlaps the host memcpy of the next
+    n = flat.numel()
+    step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
+    with torch.cuda.stream(stream):
+        for o in range(0, n, step):
+            stage[o:o + step].copy_(flat[o:o + step])
+            oflat[o:o + step].copy_(stage[o:o + step], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+    pool["events"][i] = ev
+    return ev
+
+
 def to_device(a, device, dtype=None):
     """numpy or torch -> contiguous CUDA tensor (no copy if already there)."""
     import torch

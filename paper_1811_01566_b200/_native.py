@@ -63,6 +63,8 @@ SIGNATURES = {
     "bm_das_beamform": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _P], ctypes.c_int),
     "bm_sigproc_ws_bytes": ([_I32, _I32, _I64, _I64, _I64], _I64),
     "bm_pad_traces": ([_I32, _P, _I64, _I64, _I64, _P, _I64, _P], ctypes.c_int),
+    "bm_das_beamform_range": ([ctypes.POINTER(DasGeometry), _P, _I64, _P, _I64, _I32, _I32, _I32,
+                               _I32, _P], ctypes.c_int),
     "bm_analytic_signal": ([_I32, _P, _P, _I64, _I64, _I64, _P, _I64, _P], ctypes.c_int),
     "bm_envelope": ([_I32, _P, _P, _I64, _P], ctypes.c_int),
     "bm_abs": ([_I32, _P, _P, _I64, _P], ctypes.c_int),

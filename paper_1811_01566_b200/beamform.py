@@ -168,6 +168,21 @@ class DasPlan:
     # launch, when it fits this share of the free device memory
     TABLE_MAX_FRAMES = 2
     TABLE_MEM_SHARE = 0.25
+    # a host frame's copy can be split into transmit chunks whose DAS overlaps
+    # the next chunk's copy (beamform_host); measured on cfg2, every launch
+    # pays its CTAs' setup (delay-table read, TMEM, pipeline fill) again, so
+    # 2 / 3 / 4 chunks gave 974 / 852 / 941 drop-in frames/s against 1 048
+    # for one: one chunk by default (tools/dropin_chunks.sh)
+    HOST_CHUNKS = 1
+
+    def host_overlap_ok(self, n_samples: int) -> bool:
+        """beamform_host applies: f32 frames on the TMA kernel with 16-B rows."""
+        ok = getattr(self, "_host_ok", {})
+        if n_samples not in ok:
+            ok[n_samples] = (self.dtype == np.float32 and int(n_samples) % 4 == 0
+                             and self.kernel_for(n_samples) == "tma-ws")
+            self._host_ok = ok
+        return ok[n_samples]
 
     def delay_table(self, build: bool = True):
         """The plan's device receive-delay table (the role of the reference
@@ -235,9 +250,12 @@ class DasPlan:
         return dict(zip(("frames_per_cta", "fp", "ft", "channels_per_stage", "stages",
                          "window"), list(shape)))
 
-    def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True):
+    def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True,
+                       tx_range=None, accumulate=False):
         """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
-        ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``."""
+        ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``.
+        ``tx_range=(e0, e1)`` beamforms those transmits only; ``accumulate``
+        continues the sums already in ``out`` (bm_das_beamform_range)."""
         import torch
 
         if interp not in INTERPOLATION_MODES:
@@ -274,12 +292,57 @@ class DasPlan:
         n_img = self.shape[0] * self.shape[1]
         (stream if stream is not None else torch.cuda.current_stream(self.device)).wait_event(
             self._ready)
+        e0, e1 = tx_range if tx_range is not None else (0, n_tx)
         for f0 in range(0, f, 65535):
             nf = min(65535, f - f0)
-            N.call("bm_das_beamform", ctypes.byref(g),
+            N.call("bm_das_beamform_range", ctypes.byref(g),
                    rfb[f0].data_ptr(), n_tx * n_rx * n_pad,
-                   out[f0].data_ptr(), n_img, nf, N.stream_ptr(stream))
+                   out[f0].data_ptr(), n_img, nf, int(e0), int(e1), int(bool(accumulate)),
+                   N.stream_ptr(stream))
         return out[0] if single else out
+
+
+def _tx_chunks(n_tx: int, k: int):
+    base, extra = divmod(n_tx, k)
+    lo = 0
+    for i in range(k):
+        hi = lo + base + (1 if i < extra else 0)
+        yield lo, hi
+        lo = hi
+
+
+def beamform_host(plan: DasPlan, data, interp: str = "linear", chunks: int | None = None):
+    """One HOST frame (numpy, [n_tx, n_rx, n_s]) -> device rf image, the
+    host->device copy of transmit chunk k+1 overlapping the DAS of chunk k:
+    chunk k's copy runs on a copy stream, its beamforming launch
+    (bm_das_beamform_range) waits for that copy only and continues the sums
+    of chunks < k -- so the bits equal one launch over the whole frame."""
+    import torch
+
+    from ._device import staged_copy_into
+
+    data = np.ascontiguousarray(data)
+    n_tx, n_rx, n_s = data.shape
+    if chunks is None:
+        chunks = plan.HOST_CHUNKS
+    chunks = max(1, min(int(chunks), n_tx))
+    dev = plan.device
+    key = (n_tx, n_rx, n_s)
+    cache = getattr(plan, "_host_bufs", None)
+    if cache is None or cache[0] != key:
+        rf = torch.empty((1, n_tx, n_rx, n_s), dtype=torch.float32, device=dev)
+        cache = plan._host_bufs = (key, rf, torch.cuda.Stream(dev))
+    _, rf, copy_stream = cache
+    comp = torch.cuda.current_stream(dev)
+    copy_stream.wait_stream(comp)  # the previous frame's launches read rf
+    src = torch.from_numpy(data)
+    out = torch.empty((1,) + plan.shape, dtype=torch.float32, device=dev)
+    for k, (e0, e1) in enumerate(_tx_chunks(n_tx, chunks)):
+        ev = staged_copy_into(src[e0:e1], rf[0, e0:e1], copy_stream)
+        comp.wait_event(ev)
+        plan.beamform_batch(rf, interp, out=out, stream=comp, tx_range=(e0, e1),
+                            accumulate=k > 0)
+    return out[0]
 
 
 def das_beamform(frame: RfFrame, ctx, grid, apod: ApodizationSpec = ApodizationSpec(),
@@ -294,8 +357,10 @@ def das_beamform(frame: RfFrame, ctx, grid, apod: ApodizationSpec = ApodizationS
     if plan is None or not plan.matches(ctx, grid, apod, dtype, frame.n_rx):
         plan = DasPlan(ctx, grid, apod, dtype, frame.n_rx)
     host = not _is_torch(frame.data)
-    data = to_device(frame.data, plan.device)
-    img = plan.beamform_batch(data, interp)
+    if host and plan.host_overlap_ok(frame.n_samples):
+        img = beamform_host(plan, frame.data, interp)  # copy/DAS overlap by transmit chunk
+    else:
+        img = plan.beamform_batch(to_device(frame.data, plan.device), interp)
     return BmodeImage(img.cpu().numpy() if host else img, stage="rf", grid=grid)
 
 

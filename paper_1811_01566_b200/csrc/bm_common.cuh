@@ -61,7 +61,8 @@ int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);
 // returns -1 when this launch cannot use the TMA kernel (caller falls back)
 int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
-                   int64_t out_stride, int n_frames, cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid
+                   int64_t out_stride, int n_frames, int e_begin, int e_end, int accumulate,
+                   cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid
 
 // DAS kernel selection: 0 auto (TMA where it applies, else generic), 1 generic
 inline int das_kernel_choice() { return debug_override(BM_DBG_DAS_KERNEL); }

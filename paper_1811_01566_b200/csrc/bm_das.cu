@@ -33,6 +33,8 @@ struct DasArgs {
   int64_t rf_stride;
   void* out;
   int64_t out_stride;
+  int e_begin, e_end;  // transmits of this launch
+  int accumulate;      // continue the sums already in `out`
 };
 
 template <typename T>
@@ -102,8 +104,9 @@ __global__ void __launch_bounds__(TZ * kTileX) das_kernel(const DasArgs a) {
 
   const T* __restrict__ rf = reinterpret_cast<const T*>(a.rf) + (int64_t)blockIdx.y * a.rf_stride;
   const T* __restrict__ t0s = reinterpret_cast<const T*>(g.t0_smp);
-  T acc = T(0);
-  for (int e = 0; e < g.n_tx; ++e) {
+  T* __restrict__ outp = reinterpret_cast<T*>(a.out) + (int64_t)blockIdx.y * a.out_stride + p;
+  T acc = a.accumulate && valid ? *outp : T(0);
+  for (int e = a.e_begin; e < a.e_end; ++e) {
     T txd;
     if (PW) {
       const T ca = reinterpret_cast<const T*>(g.cos_a)[e];
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(TZ * kTileX) das_kernel(const DasArgs a) {
       }
     }
   }
-  if (valid) reinterpret_cast<T*>(a.out)[(int64_t)blockIdx.y * a.out_stride + p] = acc;
+  if (valid) *outp = acc;
 }
 
 // beamform.py:66-81, in f64: active iff |elem_x[m] - x| <= z / (2 F).
@@ -269,25 +272,36 @@ extern "C" int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_st
   return -1;
 }
 
-extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
-                               void* out, int64_t out_frame_stride, int32_t n_frames,
-                               void* stream) {
+extern "C" int bm_das_beamform_range(const bm_das_geometry* g, const void* rf,
+                                     int64_t rf_frame_stride, void* out, int64_t out_frame_stride,
+                                     int32_t n_frames, int32_t e_begin, int32_t e_end,
+                                     int32_t accumulate, void* stream) {
   int rc = bm::check_geometry(g);
   if (rc) return rc;
   if (!rf || !out || n_frames < 0 || n_frames > 65535) return BM_ERR_INVALID_ARGUMENT;
+  if (e_begin < 0 || e_end > g->n_tx || e_begin >= e_end) return BM_ERR_INVALID_ARGUMENT;
   if (n_frames == 0) return BM_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int choice = bm::das_kernel_choice();
   if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride)) {
-    rc = bm::das_tma_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, s);
+    rc = bm::das_tma_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, e_begin,
+                            e_end, accumulate, s);
     if (rc >= 0) return rc;  // -1: unaligned RF pointer etc. -> generic kernel
   }
-  bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride};
+  bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride, e_begin, e_end, accumulate};
   if (g->dtype == BM_F32)
     return g->scheme == BM_PW ? bm::launch_p<float, true>(a, n_frames, s)
                               : bm::launch_p<float, false>(a, n_frames, s);
   return g->scheme == BM_PW ? bm::launch_p<double, true>(a, n_frames, s)
                             : bm::launch_p<double, false>(a, n_frames, s);
+}
+
+extern "C" int bm_das_beamform(const bm_das_geometry* g, const void* rf, int64_t rf_frame_stride,
+                               void* out, int64_t out_frame_stride, int32_t n_frames,
+                               void* stream) {
+  if (!g) return BM_ERR_INVALID_ARGUMENT;
+  return bm_das_beamform_range(g, rf, rf_frame_stride, out, out_frame_stride, n_frames, 0,
+                               g->n_tx, 0, stream);
 }
 
 // Copy n_traces traces of n_samples samples (row pitch src_pitch) into rows of

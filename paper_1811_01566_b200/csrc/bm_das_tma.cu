@@ -41,6 +41,8 @@ struct TmaArgs {
   float* out;
   int64_t out_stride;
   int n_frames;
+  int e_begin, e_end;  // transmits of this launch (the whole scheme by default)
+  int accumulate;      // 1: continue the sums already in `out` (a later transmit range)
   int frames_per_cta;
   int W;          // samples per channel window (multiple of 32: 128-B aligned rows)
   int nst;        // pipeline stages (2 .. kTmaMaxStages)
@@ -381,13 +383,14 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   const int f_begin = blockIdx.y * a.frames_per_cta;
   const int f_count = min(a.frames_per_cta, a.n_frames - f_begin);
   const int n_pass = (f_count + FPP - 1) / FPP;
-  int Q = n_pass * n_tx * n_chunks;  // passes x transmits x stages
-  int e_first = 0, e_last = n_tx - 1;
+  const int e_lo = a.e_begin, e_hi = a.e_end;
+  int Q = n_pass * (e_hi - e_lo) * n_chunks;  // passes x transmits x stages
+  int e_first = e_lo, e_last = e_hi - 1;
   if (SKIP) {
     // per-transmit stage range over the active channels; an all-zero tile
-    // still runs transmit 0's first stage (its terms are zeros)
+    // still runs its first transmit's first stage (its terms are zeros)
     const int elo = espan[0], ehi = espan[1];
-    for (int e = tid; e < n_tx; e += NTH) {
+    for (int e = e_lo + tid; e < e_hi; e += NTH) {
       const int jlo = max(0, elo - rxb[e]), jhi = min(n_rx - 1, ehi - rxb[e]);
       cblo[e] = jlo <= jhi ? jlo / TJC : 1;
       cbhi[e] = jlo <= jhi ? jhi / TJC : 0;
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
     __syncthreads();
     int tot = 0;
     e_first = -1;
-    for (int e = 0; e < n_tx; ++e)
+    for (int e = e_lo; e < e_hi; ++e)
       if (cblo[e] <= cbhi[e]) {
         tot += cbhi[e] - cblo[e] + 1;
         if (e_first < 0) e_first = e;
@@ -403,9 +406,9 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
       }
     if (e_first < 0) {
       __syncthreads();
-      if (tid == 0) cblo[0] = cbhi[0] = 0;
+      if (tid == 0) cblo[e_lo] = cbhi[e_lo] = 0;
       __syncthreads();
-      e_first = e_last = 0;
+      e_first = e_last = e_lo;
       tot = 1;
     }
     Q = n_pass * tot;
@@ -413,13 +416,13 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   // stage cursor: (pass, transmit, chunk); SKIP walks each transmit's range
   auto advance = [&](Cursor& c) {
     if (!SKIP) {
-      c.next(n_chunks, n_tx);
+      c.next(n_chunks, e_lo, e_hi);
       return;
     }
     if (++c.cb > cbhi[c.e]) {
       do {
-        if (++c.e == n_tx) {
-          c.e = 0;
+        if (++c.e == e_hi) {
+          c.e = e_lo;
           ++c.fl;
         }
       } while (cblo[c.e] > cbhi[c.e]);
@@ -493,8 +496,23 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
     const VT M2 = L::splat(kMagic), NM2 = L::splat(-kMagic);
     const VT ONE2 = L::splat(1.0f), HALF2 = L::splat(0.5f);
     VT acc[FT];
+    // sums start at +0, or -- for a later transmit range of the same frames --
+    // at the values the previous launch stored (exact: the same f32 sums
+    // continue in the same e -> j order)
+    auto start_acc = [&](int fl_pass) {
 #pragma unroll
-    for (int i = 0; i < FT; ++i) acc[i] = L::splat(0.0f);  // +0.0f
+      for (int i = 0; i < FT; ++i) {
+        acc[i] = L::splat(0.0f);  // +0.0f
+        const int fl = fl_pass * FPP + slot * FT + i;
+        if (a.accumulate && col < g.n_x && fl < f_count) {
+          const float* fo = a.out + (int64_t)(f_begin + fl) * a.out_stride;
+          const float oA = rowA < g.n_z ? fo[(int64_t)rowA * g.n_x + col] : 0.0f;
+          const float oB = rowB < g.n_z ? fo[(int64_t)rowB * g.n_x + col] : 0.0f;
+          acc[i] = L::make(oA, oB);
+        }
+      }
+    };
+    start_acc(0);
     VT txd = acc[0], t0e2 = acc[0];
     // the thread's frame i > 0 sits i frame planes ({G, W} floats) after frame 0
     const uint32_t FOFF = (uint32_t)(G * W) * 4u;
@@ -610,8 +628,8 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
             if (rowA < g.n_z) a.out[fo + (int64_t)rowA * g.n_x + col] = oA;
             if (rowB < g.n_z) a.out[fo + (int64_t)rowB * g.n_x + col] = oB;
           }
-          acc[i] = L::splat(0.0f);
         }
+        start_acc(cur.fl + 1);
       }
       advance(cur);
       if (++s == nst) {
@@ -801,7 +819,8 @@ int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape) {
 }
 
 int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
-                   int64_t out_stride, int n_frames, cudaStream_t s) {
+                   int64_t out_stride, int n_frames, int e_begin, int e_end, int accumulate,
+                   cudaStream_t s) {
   if (((uintptr_t)rf & 15) != 0) return -1;  // caller falls back
   TmaChoice c;
   if (!tma_choose(g, n_frames, c)) return -1;
@@ -822,7 +841,8 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  TmaArgs a{g, (float*)out, out_stride, n_frames, fpc, W, nst, tma_cols(g), tma_ls(g)};
+  TmaArgs a{g,   (float*)out, out_stride, n_frames,    e_begin,   e_end,
+            accumulate, fpc,  W,    nst,        tma_cols(g), tma_ls(g)};
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
 #define BM_TMA_ROW(J, WT)                                                                  \

@@ -90,12 +90,13 @@ __device__ __forceinline__ void cp_async_wait1() {
 // incrementally (no integer division in the loop).  T = fl * n_tx + e.
 struct Cursor {
   int fl, e, cb, T;
-  __device__ __forceinline__ void next(int n_chunks, int n_tx) {
+  // transmits e_lo .. e_hi - 1 of every pass (a launch may cover a range)
+  __device__ __forceinline__ void next(int n_chunks, int e_lo, int e_hi) {
     if (++cb == n_chunks) {
       cb = 0;
       ++T;
-      if (++e == n_tx) {
-        e = 0;
+      if (++e == e_hi) {
+        e = e_lo;
         ++fl;
       }
     }
