@@ -1,19 +1,35 @@
-# Per-config bench lines (current kernels) into gpurun_out/configs/, then the
-# DAS GPU tests.  Run under gpurun after the build.
-set -u
+# Per-config bench lines (BASELINE configs, paper presets, weighted and
+# nearest variants) into gpurun_out/configs/, one JSON line each.
 mkdir -p gpurun_out/configs
-b() { name=$1; shift; timeout 600 python bench.py --no-cpu "$@" > gpurun_out/configs/$name.log 2>&1
-  tail -1 gpurun_out/configs/$name.log > gpurun_out/configs/bench_$name.jsonl
-  echo "[$name] $(tail -1 gpurun_out/configs/$name.log | cut -c1-200)"; }
-b cfg2 --steps 20
-b cfg1 --config cfg1 --steps 20
-b cfg3 --config cfg3 --frames 8 --steps 10 --no-e2e
-b cfg5 --config cfg5 --steps 5
-b cfg4 --frames 256 --steps 4 --no-e2e
-b cfg2_nearest --interp nearest --steps 20 --no-e2e
-b cfg1_nearest --config cfg1 --interp nearest --steps 20 --no-e2e
-
-b sta_paper --config sta-paper --steps 10 --no-e2e
-b sta_paper_nearest --config sta-paper --interp nearest --steps 10 --no-e2e
-b pwi_paper --config pwi-paper --steps 20 --no-e2e
-b cfg2_hann_f15 --window hann --f-number 1.5 --steps 20 --no-e2e
+run() {  # $1 = name, rest = bench args
+  n=$1; shift
+  timeout 600 python bench.py --steps 20 --no-cpu --no-stai "$@" > gpurun_out/configs/$n.log 2>&1
+  tail -1 gpurun_out/configs/$n.log > gpurun_out/configs/$n.jsonl
+  python - "$n" <<'PY'
+import json, sys
+n = sys.argv[1]
+try:
+    d = json.loads(open(f"gpurun_out/configs/{n}.jsonl").read())
+    r = d.get("roofline") or {}
+    print(n, d["value"], d.get("stages_ms_per_frame"), r.get("bound"), r.get("frac"),
+          (d.get("e2e") or {}).get("value"))
+except Exception as exc:
+    print(n, "FAILED", exc)
+PY
+}
+run cfg2 --config cfg2
+run cfg2_nearest --config cfg2 --interp nearest
+run cfg1 --config cfg1
+run cfg1_nearest --config cfg1 --interp nearest
+run cfg3 --config cfg3 --frames 8
+run cfg4_256 --config cfg2 --frames 256 --steps 5 --no-e2e
+run sta_paper --config sta-paper
+run sta_paper_nearest --config sta-paper --interp nearest
+run pwi_paper --config pwi-paper
+run pwi_paper_nearest --config pwi-paper --interp nearest
+run cfg2_hann --config cfg2 --window hann
+run cfg2_hann_f15 --config cfg2 --window hann --f-number 1.5
+run cfg5_cols --config cfg5 --steps 5
+run cfg5_rows --config cfg5 --steps 5 --split rows
+run cfg1_fp2ft2 --config cfg1 --no-e2e --debug das_fp=2 --debug das_ft=2
+run cfg1_fpc8 --config cfg1 --no-e2e --debug das_fpc=8
