@@ -70,6 +70,8 @@ def parse():
                     help="receive apodisation window (ApodizationSpec)")
     ap.add_argument("--f-number", type=float, default=0.0,
                     help="dynamic-aperture f-number (0: all elements)")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="frame dtype (f64: the reference's oracle precision, the f64 TMA kernel)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stai", action="store_true",
                     help="skip the STAI blocks (cfg1 / cfg3) of the default cfg2 run")
@@ -306,13 +308,18 @@ def das_roofline(eng, ctx, grid, n_s, B, das_ms, interp, clk, n_sm, peaks, workl
         ops = (5.0 / ft + 4.0) if interp == "linear" else (3.0 / ft + 1.0)
     else:
         ops = (7.0 / ft + 4.0) if interp == "linear" else (3.0 / ft + 2.0)
-    gb = 8 if interp == "linear" else 4
+    f64 = np.dtype(eng.plan.dtype) == np.float64
+    esz = 8 if f64 else 4
+    gb = 2 * esz if interp == "linear" else esz
+    # FP32: 128 lane-ops/clk/SM (FADD2/FFMA2); FP64: 64 (DADD/DMUL at 2
+    # warp-instr/clk/SM, profiles/r02_microbench.json)
+    lane_rate = 64 if f64 else 128
     clk_hz = sm_mhz * 1e6
-    t_fp32 = contrib * ops / (n_sm * 128 * clk_hz)
+    t_fp32 = contrib * ops / (n_sm * lane_rate * clk_hz)
     t_lds = contrib * gb / (n_sm * 128 * clk_hz)
     t = das_ms / 1000.0
-    frame_bytes = ctx.n_tx * n_rx * n_s * 4
-    img_bytes = grid.n_z * grid.n_x * 4
+    frame_bytes = ctx.n_tx * n_rx * n_s * esz
+    img_bytes = grid.n_z * grid.n_x * esz
     hbm_bytes = B * (frame_bytes + img_bytes)
     hbm_peak = peaks.get("hbm_gbs", 6450.0)
     traffic = None
@@ -327,9 +334,10 @@ def das_roofline(eng, ctx, grid, n_s, B, das_ms, interp, clk, n_sm, peaks, workl
         peak, unit = n_sm * 128 * clk_hz / 1e9, "GB/s"
         per = f"{gb} B gathered per contribution"
     else:
-        bound, achieved = "fp32", contrib * ops / t / 1e12
-        peak, unit = n_sm * 128 * clk_hz / 1e12, "TFLOP/s"
-        per = f"{ops:.4g} FP32 lane-ops per contribution"
+        pipe = "fp64" if f64 else "fp32"
+        bound, achieved = pipe, contrib * ops / t / 1e12
+        peak, unit = n_sm * lane_rate * clk_hz / 1e12, "TFLOP/s"
+        per = f"{ops:.4g} {pipe.upper()} lane-ops per contribution"
     return {
         "bound": bound, "achieved": round(achieved, 1 if unit == "GB/s" else 3),
         "peak": round(peak, 1 if unit == "GB/s" else 3), "unit": unit,
@@ -337,13 +345,13 @@ def das_roofline(eng, ctx, grid, n_s, B, das_ms, interp, clk, n_sm, peaks, workl
         "kernel": f"bm_das_beamform ({eng.plan.kernel_for(n_s, interp)})",
         "kernel_ms_per_launch": round(das_ms, 4),
         "algorithmic": f"{contrib} contributions per launch x {per}",
-        "peak_source": ("measured per-SM rates (profiles/r01_microbench.json: LDS.32 1 warp-instr/"
-                        "clk/SM, FADD2/FFMA2 128 lane-ops/clk/SM) x %d SMs x %.0f MHz sampled "
-                        "during the run" % (n_sm, sm_mhz)),
+        "peak_source": ("measured per-SM rates (profiles/r02_microbench.json: LDS 128 B/clk/SM, "
+                        "FADD2/FFMA2 128 and DADD/DMUL 64 lane-ops/clk/SM) x %d SMs x %.0f MHz "
+                        "sampled during the run" % (n_sm, sm_mhz)),
         "launch_shape": shape,
         "t_smem_gather_roof_ms": round(t_lds * 1000, 4),
-        "t_fp32_roof_ms": round(t_fp32 * 1000, 4),
-        "fp32_lane_ops_per_contribution": round(ops, 4),
+        "t_fp_pipe_roof_ms": round(t_fp32 * 1000, 4),
+        "fp_lane_ops_per_contribution": round(ops, 4),
         "hbm": {"achieved": round(hbm_bytes / t / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(hbm_bytes / t / 1e9 / hbm_peak, 4),
                 "algorithmic_bytes_per_launch": hbm_bytes,
@@ -548,13 +556,17 @@ def main():
         return run_cfg5(args, ctx, grid, n_s, rank, world, local, dev)
 
     B = args.frames
-    host = synth_frames(ctx, n_s, B, seed0=rank * B)
+    fdt = np.float32 if args.dtype == "f32" else np.float64
+    host = synth_frames(ctx, n_s, B, seed0=rank * B).astype(fdt)
     apod = bm.ApodizationSpec(args.window, args.f_number)
-    eng = bm.engine.BmodeEngine(ctx, grid, apod=apod, interp=args.interp, dtype=np.float32)
+    eng = bm.engine.BmodeEngine(ctx, grid, apod=apod, interp=args.interp, dtype=fdt)
     if not eng.plan.uniform:
         WORKLOAD = WORKLOAD + f", {args.window} F={args.f_number:g}"
+    if args.dtype == "f64":
+        WORKLOAD = WORKLOAD + ", f64"
+        frame_bytes, img_bytes = 2 * frame_bytes, 2 * img_bytes
     rf = torch.from_numpy(host).to(dev)
-    out = torch.empty((B, grid.n_z, grid.n_x), dtype=torch.float32, device=dev)
+    out = torch.empty((B, grid.n_z, grid.n_x), dtype=eng.tdtype, device=dev)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks = {}
     try:
@@ -610,7 +622,7 @@ def main():
                             WORKLOAD)
 
     stai = None
-    if not args.no_stai and args.config == "cfg2":
+    if not args.no_stai and args.config == "cfg2" and args.dtype == "f32":
         del rf
         torch.cuda.empty_cache()
         clocks2 = ClockSampler(local)
@@ -627,14 +639,14 @@ def main():
         if world > 1:
             torch.distributed.destroy_process_group()
         return
-    if e2e is not None and world == 1:
+    if e2e is not None and world == 1 and args.dtype == "f32":
         e2e["dropin_per_frame_fps"] = round(dropin_fps(ctx, grid, host, args.interp), 1)
         e2e["dropin_note"] = ("one frame per call through the reference-facing operator chain "
                               "(numpy in, numpy display out, pageable copies); value above is "
                               "the batched engine from pinned memory")
 
     cpu = None
-    if not args.no_cpu and args.cpu_seconds > 0 and world == 1:  # rank 0 at N=1 only
+    if not args.no_cpu and args.cpu_seconds > 0 and world == 1 and args.dtype == "f32":
         fps, cores, n, el = cpu_reference(ctx, grid, host[:4], args.cpu_seconds, args.interp)
         cpu = {"value": round(fps, 4), "unit": "frames/s", "cores": cores, "kind": "port",
                "sample": f"{n} {args.config} frames in {el:.1f}s: oracle/ C DAS (pthreads) + "
@@ -644,7 +656,7 @@ def main():
         "metric": "B-mode frames/sec", "value": round(value, 2), "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic wire phantom + N(0,0.01)",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic wire phantom + N(0,0.01)",
         "config": {"workload": WORKLOAD, "frames_per_gpu_per_step": B,
                    "global_frames_per_step": B * world, "parallelism": f"frames over {world} GPU",
                    "l2": f"inputs {B * frame_bytes / 1e6:.0f} MB per GPU > 126 MB L2, no flush"},

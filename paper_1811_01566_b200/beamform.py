@@ -222,12 +222,14 @@ class DasPlan:
         g.interp = N.BM_NEAREST if interp == "nearest" else N.BM_LINEAR
         return g
 
-    KERNELS = {0: "generic", 1: "smem", 2: "tmem-scalar", 3: "tmem-pair", 4: "tmem-hybrid",
-               5: "tma-ws"}
+    KERNELS = {0: "generic", 5: "tma-ws", 6: "tma64"}
 
     def _padded(self, n_samples: int, fast: bool) -> int:
-        """Trace length a launch runs with (f32 fast path: rows padded to 16 B)."""
-        return -(-int(n_samples) // 4) * 4 if fast and self.dtype == np.float32 else int(n_samples)
+        """Trace length a launch runs with (fast paths: rows padded to 16 B)."""
+        if not fast:
+            return int(n_samples)
+        q = 4 if self.dtype == np.float32 else 2
+        return -(-int(n_samples) // q) * q
 
     def kernel_for(self, n_samples: int, interp: str = "linear", fast: bool = True) -> str:
         """Name of the CUDA kernel a launch with this trace length would use."""
@@ -272,17 +274,17 @@ class DasPlan:
         if out is None:
             out = torch.empty((f,) + self.shape, dtype=rfb.dtype, device=self.device)
         n_pad = n_s
-        if fast and self.dtype == np.float32 and (n_s % 4 or rfb.stride(-1) != 1
-                                                   or not rfb.is_contiguous()):
-            # the TMA kernel wants 16-B trace rows: copy into rows of a multiple
-            # of 4 samples, zero tail (bm_pad_traces; bitwise the same result)
-            n_pad = -(-n_s // 4) * 4
+        if fast and (n_s != self._padded(n_s, True) or not rfb.is_contiguous()):
+            # the TMA kernels want 16-B trace rows: copy into rows of a multiple
+            # of 4 (f32) / 2 (f64) samples, zero tail (bm_pad_traces; bitwise
+            # the same result)
+            n_pad = self._padded(n_s, True)
             if rfb.stride(-1) != 1 or rfb.stride(-2) * n_rx != rfb.stride(-3) or \
                     rfb.stride(-3) * n_tx != rfb.stride(0):
                 rfb = rfb.contiguous()
             padded = torch.empty((f, n_tx, n_rx, n_pad), dtype=rfb.dtype, device=self.device)
-            N.call("bm_pad_traces", N.BM_F32, rfb.data_ptr(), rfb.stride(-2), f * n_tx * n_rx,
-                   n_s, padded.data_ptr(), n_pad, N.stream_ptr(stream))
+            N.call("bm_pad_traces", N.dtype_code(self.dtype), rfb.data_ptr(), rfb.stride(-2),
+                   f * n_tx * n_rx, n_s, padded.data_ptr(), n_pad, N.stream_ptr(stream))
             rfb = padded
         elif not rfb.is_contiguous():
             rfb = rfb.contiguous()

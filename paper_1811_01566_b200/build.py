@@ -44,7 +44,7 @@ def up_to_date() -> bool:
 # Files whose results must be bitwise equal to the reference: no FMA
 # contraction anywhere (ptxas would otherwise fuse mul.rn.f32x2 + add.rn.f32x2
 # into FFMA2, changing the rounding of the DAS accumulation).
-NO_FMAD = {"bm_das.cu", "bm_das_tma.cu"}
+NO_FMAD = {"bm_das.cu", "bm_das_tma.cu", "bm_das_tma64.cu"}
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -64,6 +64,13 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                    int64_t out_stride, int n_frames, int e_begin, int e_end, int accumulate,
                    cudaStream_t s);  // 0 scalar, 1 pair, 2 hybrid
 
+// f64 twin of the TMA kernel (bm_das_tma64.cu)
+int das_tma64_eligible(const bm_das_geometry& g, int64_t rf_stride);
+int das_tma64_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);
+int das_tma64_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
+                     int64_t out_stride, int n_frames, int e_begin, int e_end, int accumulate,
+                     cudaStream_t s);
+
 // DAS kernel selection: 0 auto (TMA where it applies, else generic), 1 generic
 inline int das_kernel_choice() { return debug_override(BM_DBG_DAS_KERNEL); }
 

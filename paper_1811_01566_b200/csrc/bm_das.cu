@@ -260,6 +260,7 @@ extern "C" int bm_das_select(const bm_das_geometry* g, int64_t rf_frame_stride) 
   if (bm::check_geometry(g)) return -1;
   const int choice = bm::das_kernel_choice();
   if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride)) return 5;
+  if (choice == 0 && bm::das_tma64_eligible(*g, rf_frame_stride)) return 6;
   return 0;
 }
 
@@ -269,6 +270,8 @@ extern "C" int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_st
   const int choice = bm::das_kernel_choice();
   if (choice == 0 && bm::das_tma_eligible(*g, rf_frame_stride))
     return bm::das_tma_shape(*g, n_frames, shape);
+  if (choice == 0 && bm::das_tma64_eligible(*g, rf_frame_stride))
+    return bm::das_tma64_shape(*g, n_frames, shape);
   return -1;
 }
 
@@ -287,6 +290,11 @@ extern "C" int bm_das_beamform_range(const bm_das_geometry* g, const void* rf,
     rc = bm::das_tma_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, e_begin,
                             e_end, accumulate, s);
     if (rc >= 0) return rc;  // -1: unaligned RF pointer etc. -> generic kernel
+  }
+  if (choice == 0 && bm::das_tma64_eligible(*g, rf_frame_stride)) {
+    rc = bm::das_tma64_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, e_begin,
+                              e_end, accumulate, s);
+    if (rc >= 0) return rc;
   }
   bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride, e_begin, e_end, accumulate};
   if (g->dtype == BM_F32)

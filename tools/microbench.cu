@@ -38,10 +38,12 @@ __global__ void bench(int salt) {
   __syncthreads();
   u64 v[8];
   float f[8];
+  double dv[8];
   uint32_t addr[8];
   for (int i = 0; i < 8; ++i) {
     v[i] = (u64)(tid + i) * 0x3f8000013f800001ull;
     f[i] = (float)(tid + i);
+    dv[i] = (double)(tid + i);
     // conflict-free gather pattern: lanes spread over a 32-word window
     addr[i] = (uint32_t)__cvta_generic_to_shared(sm) + 4u * (uint32_t)((tid * 7 + i * 37) & 8191);
   }
@@ -65,6 +67,15 @@ __global__ void bench(int salt) {
         asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(x) : "r"(addr[0] & ~127u));
         f[i] += x;
       }
+      if (KIND == 6) dv[i] = __dadd_rn(dv[i], 1.0);                  // DADD
+      if (KIND == 7) dv[i] = __dmul_rn(dv[i], 1.0000001);            // DMUL
+      if (KIND == 8) {  // LDS.64, lanes on consecutive 8-B words (2 wavefronts)
+        double x;
+        asm volatile("ld.volatile.shared.f64 %0, [%1];"
+                     : "=d"(x)
+                     : "r"(((uint32_t)__cvta_generic_to_shared(sm) + 8u * (uint32_t)((tid & 31) + 64 * i)) ^ (uint32_t)(it & 1) * 512u));
+        dv[i] += x;
+      }
       if (KIND == 4) {                                              // LDS.64
         u64 x;
         asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(x) : "r"(addr[i] & ~7u));
@@ -76,7 +87,7 @@ __global__ void bench(int salt) {
   __syncthreads();  // the slowest warp ends the interval
   const long long t1 = clock64();
   u64 acc = 0;
-  for (int i = 0; i < 8; ++i) acc ^= v[i] ^ (u64)__float_as_uint(f[i]);
+  for (int i = 0; i < 8; ++i) acc ^= v[i] ^ (u64)__float_as_uint(f[i]) ^ (u64)__double_as_longlong(dv[i]);
   if (acc == 0x1234567ull) g_sink = acc;
   if (tid == 0) g_cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
 }
@@ -84,13 +95,15 @@ __global__ void bench(int salt) {
 int main() {
   int dev = 0, sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const char* names[6] = {"fadd2", "fadd", "ffma2_rz", "lds32_gather", "lds64", "lds32_bcast"};
+  const char* names[9] = {"fadd2", "fadd", "ffma2_rz", "lds32_gather", "lds64", "lds32_bcast",
+                          "dadd", "dmul", "lds64_consecutive"};
   printf("{\"sm_count\": %d", sms);
-  for (int kind = 0; kind < 6; ++kind) {
+  for (int kind = 0; kind < 9; ++kind) {
     for (int warps : {4, 8, 16}) {
       const int threads = 32 * warps;
       auto fn = kind == 0 ? bench<0> : kind == 1 ? bench<1> : kind == 2 ? bench<2>
-               : kind == 3 ? bench<3> : kind == 4 ? bench<4> : bench<5>;
+               : kind == 3 ? bench<3> : kind == 4 ? bench<4> : kind == 5 ? bench<5>
+               : kind == 6 ? bench<6> : kind == 7 ? bench<7> : bench<8>;
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
       fn<<<sms, threads, 32768>>>(1);
       fn<<<sms, threads, 32768>>>(2);
