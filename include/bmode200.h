@@ -150,8 +150,9 @@ int bm_das_launch_shape(const bm_das_geometry* g, int64_t rf_frame_stride, int32
  * build (stream-ordered, one launch).  A launch with g->rx_table set reads
  * each CTA's 128 pixel pairs x n_elements delays from it instead of
  * evaluating fs*(sqrt(dx^2+z^2)/c) per CTA -- the dominant per-CTA cost of a
- * one-frame launch.  Valid for the geometry (positions, c, fs, tile shape)
- * it was built from.  0 / BM_ERR_UNSUPPORTED when the TMA kernel does not
+ * one-frame launch (f32: n_el x n_px f32 pairs; f64: n_el x n_px f64, the
+ * f64 kernel's one pixel per thread; `table` is then a double* cast).  Valid
+ * for the geometry (positions, c, fs, tile shape) it was built from.  0 / BM_ERR_UNSUPPORTED when the TMA kernel does not
  * apply. */
 int64_t bm_das_table_bytes(const bm_das_geometry* g);
 int bm_das_build_table(const bm_das_geometry* g, float* table, void* stream);

@@ -191,7 +191,7 @@ class DasPlan:
         import torch
 
         tab = getattr(self, "_table", None)
-        if tab is not None or not build or self.dtype != np.float32:
+        if tab is not None or not build:
             return tab
         if getattr(self, "_table_refused", False):
             return None
@@ -288,7 +288,7 @@ class DasPlan:
             rfb = padded
         elif not rfb.is_contiguous():
             rfb = rfb.contiguous()
-        if fast and f <= self.TABLE_MAX_FRAMES and self.dtype == np.float32:
+        if fast and f <= self.TABLE_MAX_FRAMES:
             self.delay_table()
         g = self.geometry(n_pad, interp, fast)
         n_img = self.shape[0] * self.shape[1]

@@ -67,6 +67,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
 // f64 twin of the TMA kernel (bm_das_tma64.cu)
 int das_tma64_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tma64_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);
+int das_table64_build(const bm_das_geometry& g, double* table, cudaStream_t s);
 int das_tma64_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, void* out,
                      int64_t out_stride, int n_frames, int e_begin, int e_end, int accumulate,
                      cudaStream_t s);

@@ -904,13 +904,18 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
 }  // namespace bm
 
 extern "C" int64_t bm_das_table_bytes(const bm_das_geometry* g) {
-  if (!g || g->dtype != BM_F32 || g->n_elements < 1 || g->n_z < 1 || g->n_x < 1) return 0;
+  if (!g || g->n_elements < 1 || g->n_z < 1 || g->n_x < 1) return 0;
+  if (g->dtype == BM_F64)  // f64 delays of each consumer thread's pixel
+    return (int64_t)bm::tma_tiles(*g) * g->n_elements * 256 * 8;
+  if (g->dtype != BM_F32) return 0;
   return (int64_t)bm::tma_tiles(*g) * g->n_elements * 128 * 8;
 }
 
 extern "C" int bm_das_build_table(const bm_das_geometry* g, float* table, void* stream) {
   if (!g || !table || !g->elem_x || !g->x_pos || !g->z_pos) return BM_ERR_INVALID_ARGUMENT;
   if (bm_das_table_bytes(g) <= 0) return BM_ERR_UNSUPPORTED;
+  if (g->dtype == BM_F64)
+    return bm::das_table64_build(*g, reinterpret_cast<double*>(table), (cudaStream_t)stream);
   const dim3 grid((unsigned)bm::tma_tiles(*g), (unsigned)std::min(g->n_elements, 16));
   bm::das_table_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*g, bm::tma_ls(*g),
                                                                reinterpret_cast<float2*>(table));

@@ -64,6 +64,34 @@ __device__ __forceinline__ double words_f64(uint32_t lo, uint32_t hi) {
   return __hiloint2double((int)hi, (int)lo);
 }
 
+// exact f64 receive delay fs*(sqrt(dx*dx + z*z)/c) of element m (beamform.py:211-216)
+__device__ __forceinline__ double rx_delay64(const bm_das_geometry& g, int m, double px,
+                                             double pz) {
+  using O = R<double>;
+  const double dx = g.elem_x[m] - px;
+  return O::mul(g.sampling_frequency,
+                O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pz, pz))), g.speed_of_sound));
+}
+
+// f64 plan table: table[tile][m][i], i = consumer thread (i < 128: pixel A of
+// pair i, else pixel B of pair i - 128)
+__global__ void __launch_bounds__(256) das_table64_kernel(const bm_das_geometry g, int ls,
+                                                          double* __restrict__ table) {
+  const int i = threadIdx.x;
+  const PairPos pp(g, ls, blockIdx.x, i & 127);
+  const int row = (i >> 7) ? pp.rowB : pp.rowA;
+  const double px = g.x_pos[min(pp.col, g.n_x - 1)], pz = g.z_pos[min(row, g.n_z - 1)];
+  double* tb = table + (int64_t)blockIdx.x * g.n_elements * 256 + i;
+  for (int m = blockIdx.y; m < g.n_elements; m += gridDim.y)
+    tb[(int64_t)m * 256] = rx_delay64(g, m, px, pz);
+}
+
+int das_table64_build(const bm_das_geometry& g, double* table, cudaStream_t s) {
+  const dim3 grid((unsigned)tma_tiles(g), (unsigned)std::min(g.n_elements, 16));
+  das_table64_kernel<<<grid, 256, 0, s>>>(g, tma_ls(g), table);
+  return cuda_status();
+}
+
 template <bool PW, bool LINEAR, bool T0, bool IDMAP, bool WT>
 __global__ void __launch_bounds__(288, 1)
     das_tma64_kernel(const __grid_constant__ CUtensorMap rf_map, const Tma64Args a) {
@@ -133,11 +161,22 @@ __global__ void __launch_bounds__(288, 1)
   int wlo = 0, whi = n_el - 1;
   int i0 = 0, i1 = n_el - 1;  // WT: the pixel's active span
   if (!producer) {
-    // exact receive delays of the pixel (beamform.py:211-216) -> TMEM
-    for (int m = 0; m < n_el; ++m) {
-      const double dx = g.elem_x[m] - px;
-      const double d = O::mul(fs, O::div(O::sqrt(O::add(O::mul(dx, dx), O::mul(pz, pz))), c));
-      tm_st_f64(tlane + 2 * m, d);
+    if (g.rx_table) {
+      // the plan's table (bm_das_build_table): [tile][m][256 consumer threads]
+      const double* tb = reinterpret_cast<const double*>(g.rx_table) +
+                         (int64_t)blockIdx.x * n_el * NC + cidx;
+      int m = 0;
+      for (; m + 15 < n_el; m += 16) {
+        double d[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) d[u] = __ldcs(tb + (int64_t)(m + u) * NC);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) tm_st_f64(tlane + 2 * (m + u), d[u]);
+      }
+      for (; m < n_el; ++m) tm_st_f64(tlane + 2 * m, __ldcs(tb + (int64_t)m * NC));
+    } else {
+      // exact receive delays of the pixel (beamform.py:211-216) -> TMEM
+      for (int m = 0; m < n_el; ++m) tm_st_f64(tlane + 2 * m, rx_delay64(g, m, px, pz));
     }
     if (WT && g.span) {
       const int64_t p = (int64_t)rowc * g.n_x + colc;
