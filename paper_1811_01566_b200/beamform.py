@@ -329,14 +329,15 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", chunks: int | Non
         chunks = plan.HOST_CHUNKS
     chunks = max(1, min(int(chunks), n_tx))
     dev = plan.device
-    key = (n_tx, n_rx, n_s)
-    cache = getattr(plan, "_host_bufs", None)
-    if cache is None or cache[0] != key:
-        rf = torch.empty((1, n_tx, n_rx, n_s), dtype=torch.float32, device=dev)
-        cache = plan._host_bufs = (key, rf, torch.cuda.Stream(dev))
-    _, rf, copy_stream = cache
+    copy_stream = getattr(plan, "_copy_stream", None)
+    if copy_stream is None:
+        copy_stream = plan._copy_stream = torch.cuda.Stream(dev)
     comp = torch.cuda.current_stream(dev)
-    copy_stream.wait_stream(comp)  # the previous frame's launches read rf
+    # a buffer per call (plans are shared between threads); the copy stream
+    # writes it only after the allocating stream's earlier work, and every
+    # launch that reads it waits for its copies
+    rf = torch.empty((1, n_tx, n_rx, n_s), dtype=torch.float32, device=dev)
+    copy_stream.wait_stream(comp)
     src = torch.from_numpy(data)
     out = torch.empty((1,) + plan.shape, dtype=torch.float32, device=dev)
     for k, (e0, e1) in enumerate(_tx_chunks(n_tx, chunks)):

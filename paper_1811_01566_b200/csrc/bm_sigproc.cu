@@ -1025,9 +1025,9 @@ static int launch_envelope_display(const T* x, T* disp, typename PeakBits<T>::U*
         void* args[] = {(void*)&xa, (void*)&oa, (void*)&pa, (void*)&items, (void*)&per_frame,
                         (void*)&inner, (void*)&da};
         if (cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)g), dim3(256), args,
-                                        reg_smem(kDisplay, n_z), s) != cudaSuccess)
-          return BM_ERR_CUDA;
-        return cuda_status();
+                                        reg_smem(kDisplay, n_z), s) == cudaSuccess)
+          return cuda_status();
+        cudaGetLastError();  // co-residency refused (e.g. a shared GPU): two launches below
       }
     } else {
       auto k = analytic_lane_kernel<T, kDisplay>;
@@ -1036,9 +1036,9 @@ static int launch_envelope_display(const T* x, T* disp, typename PeakBits<T>::U*
       void* args[] = {(void*)&xa, (void*)&oa, (void*)&pa, (void*)&p, (void*)&items,
                       (void*)&per_frame, (void*)&inner, (void*)&L, (void*)&ls, (void*)&da};
       if (cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)g), dim3(256), args, sp.smem,
-                                      s) != cudaSuccess)
-        return BM_ERR_CUDA;
-      return cuda_status();
+                                      s) == cudaSuccess)
+        return cuda_status();
+      cudaGetLastError();
     }
   }
   // envelope + peak into disp, then the display mapping in place
