@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--split", default="cols", choices=["cols", "rows"],
                     help="cfg5: split one frame by image columns (rank-local FFT, gather of "
                          "display tiles) or by depth rows (gather of RF rows, K2 on rank 0)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="cfg5 column split: envelope kernel writes tiles into the destination's "
+                         "NVLink peer buffer (peer), or one NCCL gather (nccl)")
     ap.add_argument("--window", default="rectangular", choices=["rectangular", "hann"],
                     help="receive apodisation window (ApodizationSpec)")
     ap.add_argument("--f-number", type=float, default=0.0,
@@ -221,6 +224,16 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
             if full is not None:
                 launches[0] += 1
                 return P.envelope_display(full, 30.0)
+    elif args.transport == "peer":
+        # the envelope kernel writes each tile into rank 0's symmetric buffer
+        # over NVLink; device-side epoch flags, no collective kernel
+        peer = P.PeerTiles(split, dev)
+        slab = torch.empty((1,) + plan.shape, dtype=f32, device=dev)
+
+        def step():
+            plan.beamform_batch(frame, out=slab)
+            launches[0] += 4 + (1 + world if rank == 0 else 0)
+            return peer.step(slab[0], 30.0)
     else:
         tile = split.send_tile(f32, dev)
         recv = split.recv_tiles(f32, dev) if rank == 0 else None
@@ -264,11 +277,14 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
             "data": "synthetic wire phantom + N(0,0.01)",
             "config": {"workload": "cfg5 STAI 128el x 128tx x 4096 samples -> 2048x2048, " + (
                 "depth-row split, one gather of RF bands, envelope + display on rank 0" if rows
-                else "lateral column split, one gather of [envelope | peak] tiles, display on "
-                     "rank 0"),
+                else ("lateral column split, envelope kernel writes [envelope | peak] tiles into "
+                      "rank 0's NVLink peer buffer, device-side flags, display on rank 0"
+                      if args.transport == "peer" else
+                      "lateral column split, one NCCL gather of [envelope | peak] tiles, display "
+                      "on rank 0")),
                        ("rows_per_rank" if rows else "columns_per_rank"): split.hi - split.lo},
             "e2e": None, "gpu_launches": launches[0]}), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
@@ -543,11 +559,14 @@ def main():
     for kv in args.debug:
         k, v = kv.split("=")
         N.load().bm_debug_set(N.DEBUG_KEYS[k], int(v))
-    if world > 1:
+    if world > 1 or (args.config == "cfg5" and args.split == "cols" and args.transport == "peer"):
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())

@@ -244,6 +244,14 @@ int bm_display_tiles(int32_t dtype, const void* tiles, int32_t n_tiles, int64_t 
  * *flag (device int32) = 1 if any value is NaN or +-inf, else 0. */
 int bm_check_finite(int32_t dtype, const void* x, int64_t count, int32_t* flag, void* stream);
 
+/* Cross-GPU frame handshakes for the peer-memory (NVLink) column split:
+ * bm_signal_flag stores `value` into *flag (possibly a peer GPU's memory) with
+ * system-scope release after every earlier operation of `stream`;
+ * bm_wait_flags holds `stream` until flags[0 .. n) are all >= value
+ * (system-scope acquire).  One tiny kernel each. */
+int bm_signal_flag(int32_t* flag, int32_t value, void* stream);
+int bm_wait_flags(const int32_t* flags, int32_t n, int32_t value, void* stream);
+
 /* dynamic_adjustment as one call: bm_frame_peak then bm_display. */
 int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,
                           int32_t* status, int32_t n_frames, int64_t frame_elems,

@@ -80,6 +80,8 @@ SIGNATURES = {
                         _I32, _P, _P], ctypes.c_int),
     "bm_display_tiles": ([_I32, _P, _I32, _I64, _I64, _I64, _P, _P, _D, _P], ctypes.c_int),
     "bm_check_finite": ([_I32, _P, _I64, _P, _P], ctypes.c_int),
+    "bm_signal_flag": ([_P, _I32, _P], ctypes.c_int),
+    "bm_wait_flags": ([_P, _I32, _I32, _P], ctypes.c_int),
     "bm_frame_peak": ([_I32, _P, _P, _I32, _I64, _P], ctypes.c_int),
     "bm_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),
     "bm_dynamic_adjustment": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),

@@ -1181,6 +1181,43 @@ extern "C" int bm_check_finite(int32_t dtype, const void* x, int64_t count, int3
   return cuda_status();
 }
 
+namespace bm {
+// cross-GPU flags in NVLink peer (or local) memory: system-scope release /
+// acquire, so the data a stream wrote before a signal is visible to the GPU
+// that observes it
+__global__ void signal_flag_kernel(int32_t* flag, int32_t value) {
+  asm volatile("fence.sc.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+__global__ void wait_flags_kernel(const int32_t* flags, int32_t n, int32_t value) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      if (v >= value) break;
+      __nanosleep(128);
+    }
+  }
+  asm volatile("fence.sc.sys;" ::: "memory");
+}
+}  // namespace bm
+
+// Stream-ordered signal: after every earlier operation of `stream`,
+// *flag = value (flag may live in a peer GPU's memory).
+extern "C" int bm_signal_flag(int32_t* flag, int32_t value, void* stream) {
+  if (!flag) return BM_ERR_INVALID_ARGUMENT;
+  signal_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  return cuda_status();
+}
+
+// Stream-ordered wait: later operations of `stream` start once every
+// flags[i] >= value (i < n).
+extern "C" int bm_wait_flags(const int32_t* flags, int32_t n, int32_t value, void* stream) {
+  if (!flags || n < 1) return BM_ERR_INVALID_ARGUMENT;
+  wait_flags_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flags, n, value);
+  return cuda_status();
+}
+
 extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,
                              int64_t frame_elems, void* stream) {
   if (!e || !peak || n_frames < 1 || n_frames > 65535 || frame_elems < 0)

@@ -144,6 +144,80 @@ class LateralSplit:
         return out, status
 
 
+class PeerTiles:
+    """The column split's gather done by the envelope kernel itself, over
+    NVLink peer memory (torch symmetric memory maps every rank's receive
+    buffer into every process):
+
+      rank r:   wait until its slot is free (device-side flag)
+                bm_envelope_peak writes the slab's envelope AND its peak
+                  straight into the destination's receive row r (peer stores
+                  and a peer atomicMax -- the transfer IS the kernel's output)
+                raise ready[r] on the destination (system-scope release)
+      dst:      wait for every ready[r] (device-side acquire)
+                bm_display_tiles over the rows, then free every rank's slot
+
+    No collective kernel and no host synchronisation: frames are ordered by
+    per-rank epoch flags, so the DAS of frame e + 1 overlaps the transfer and
+    display of frame e.  Same tile layout and kernels as LateralSplit's NCCL
+    gather, so the display is the same bits."""
+
+    def __init__(self, split: "LateralSplit", device, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.split, self.dst, self.device = split, int(dst), device
+        world, me = split.world, split.rank
+        g = group if group is not None else dist.group.WORLD
+        self.recv = symm.empty((world, split.tile_stride), dtype=torch.float32, device=device)
+        # flags[0][r]: tile r ready (on dst); flags[1][0]: this rank's slot free
+        self.flags = symm.empty((2, world), dtype=torch.int32, device=device)
+        self.flags.zero_()
+        torch.cuda.synchronize(device)
+        self.h_recv = symm.rendezvous(self.recv, g)
+        self.h_flags = symm.rendezvous(self.flags, g)
+        dist.barrier(g)
+        self.tile_ptr = self.h_recv.buffer_ptrs[self.dst] + me * split.tile_stride * 4
+        self.ready_ptr = self.h_flags.buffer_ptrs[self.dst] + me * 4
+        self.free_ptrs = [p + world * 4 for p in self.h_flags.buffer_ptrs]
+        self.is_dst = me == self.dst
+        self.epoch = 0
+        self._ws = None
+
+    def step(self, rf_slab, range_db: float, out=None):
+        """One frame: this rank's slab [n_z, w] -> its tile on dst; returns
+        (display, status) on dst, None elsewhere.  Enqueued on the current
+        stream."""
+        import torch
+
+        from . import _native as N
+
+        sp = self.split
+        self.epoch += 1
+        e = self.epoch
+        n_z, w = rf_slab.shape
+        x = rf_slab.contiguous()
+        s = N.stream_ptr()
+        with torch.cuda.device(self.device):
+            lib = N.load()
+            N.call("bm_wait_flags", self.flags.data_ptr() + sp.world * 4, 1, e - 1, s)
+            nb = int(lib.bm_sigproc_ws_bytes(N.SIG_ENVELOPE_PEAK, N.BM_F32, 1, n_z, w))
+            if nb and (self._ws is None or self._ws.numel() < nb):
+                self._ws = N.workspace(nb, self.device)
+            N.call("bm_envelope_peak", N.BM_F32, x.data_ptr(), self.tile_ptr,
+                   self.tile_ptr + (sp.tile_stride - 1) * 4, 1, n_z, w,
+                   self._ws.data_ptr() if nb else None, nb, s)
+            N.call("bm_signal_flag", self.ready_ptr, e, s)
+            if not self.is_dst:
+                return None
+            N.call("bm_wait_flags", self.flags.data_ptr(), sp.world, e, s)
+            disp, status = sp.display(self.recv, range_db, out=out)
+            for p in self.free_ptrs:
+                N.call("bm_signal_flag", p, e, s)
+        return disp, status
+
+
 def row_bands(n_z: int, world: int) -> list[tuple[int, int]]:
     """[lo, hi) depth-row ranges, one per rank, sizes differing by <= 1."""
     return column_slabs(n_z, world)

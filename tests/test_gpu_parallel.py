@@ -84,3 +84,42 @@ def test_row_bands_equal_full_frame():
     disp, status = P.envelope_display(stacked, 30.0)
     assert int(status.item()) == 0
     assert torch.equal(disp, disp_full)
+
+
+def test_peer_tiles_envelope_kernel_writes_the_gather():
+    """The NVLink peer-memory form of the column split (parallel.PeerTiles):
+    bm_envelope_peak writes each rank's [envelope | peak] tile straight into
+    the destination's symmetric receive buffer, device-side epoch flags order
+    the frames, and the destination's display equals the one-GPU chain bitwise
+    -- over several back-to-back frames with no host synchronisation between
+    them.  One rank here (the peer mapping is the rank's own buffer): ranks
+    whose kernels wait on each other must not share a GPU."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ctx, grid, n_s = ME.config_geometry("cfg5", n_z=256, n_x=200)
+        split = P.LateralSplit(grid, 1, 0)
+        peer = P.PeerTiles(split, torch.device("cuda", 0))
+        full = bm.BmodeEngine(ctx, grid)
+        g = torch.Generator(device="cuda").manual_seed(9)
+        frames = [torch.randn((1, 128, 128, n_s), generator=g, device="cuda") for _ in range(3)]
+        outs = []
+        for rf in frames:
+            slab = full.plan.beamform_batch(rf)[0]
+            disp, status = peer.step(slab, 30.0)
+            outs.append((disp.clone(), status.clone()))
+        for rf, (disp, status) in zip(frames, outs):
+            assert int(status.item()) == 0
+            assert torch.equal(disp, full.reconstruct(rf)[0])
+        assert peer.epoch == 3
+    finally:
+        dist.destroy_process_group()
