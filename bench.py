@@ -212,7 +212,15 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
     frame = torch.from_numpy(synth_frames(ctx, n_s, 1, 0)).to(dev)  # replicated RF
     f32 = torch.float32
     launches = [0]
-    if rows:
+    if rows and args.transport == "peer":
+        # the DAS kernel stores this rank's rows into rank 0's frame buffer
+        # over NVLink; device-side flags, no collective kernel
+        bands = P.PeerBands(split, dev)
+
+        def step():
+            launches[0] += 3 + (2 + world if rank == 0 else 0)
+            return bands.step(plan, frame, 30.0)
+    elif rows:
         send = split.send_band(f32, dev)
         recv = split.recv_bands(f32, dev) if rank == 0 else None
         mine = send[None, : split.hi - split.lo]
@@ -276,7 +284,11 @@ def run_cfg5(args, ctx, grid, n_s, rank, world, local, dev):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic wire phantom + N(0,0.01)",
             "config": {"workload": "cfg5 STAI 128el x 128tx x 4096 samples -> 2048x2048, " + (
-                "depth-row split, one gather of RF bands, envelope + display on rank 0" if rows
+                ("depth-row split, the DAS kernel stores its rows into rank 0's NVLink peer "
+                 "frame buffer, device-side flags, envelope + display on rank 0"
+                 if args.transport == "peer" else
+                 "depth-row split, one NCCL gather of RF bands, envelope + display on rank 0")
+                if rows
                 else ("lateral column split, envelope kernel writes [envelope | peak] tiles into "
                       "rank 0's NVLink peer buffer, device-side flags, display on rank 0"
                       if args.transport == "peer" else
@@ -559,7 +571,7 @@ def main():
     for kv in args.debug:
         k, v = kv.split("=")
         N.load().bm_debug_set(N.DEBUG_KEYS[k], int(v))
-    if world > 1 or (args.config == "cfg5" and args.split == "cols" and args.transport == "peer"):
+    if world > 1 or (args.config == "cfg5" and args.transport == "peer"):
         import torch.distributed as dist
 
         torch.cuda.set_device(local)

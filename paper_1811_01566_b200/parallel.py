@@ -271,6 +271,61 @@ class RowSplit:
         return torch.cat([recv[r, : b - a] for r, (a, b) in enumerate(self.bands)], dim=0)
 
 
+class PeerBands:
+    """The depth-row split's gather done by the DAS kernel itself: rank 0's
+    frame buffer is symmetric memory mapped into every rank, and each rank's
+    bm_das_beamform stores its band's rows straight into it (NVLink peer
+    stores); flags as in PeerTiles, then rank 0 runs the fused envelope +
+    display of the whole frame."""
+
+    def __init__(self, split: "RowSplit", device, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.split, self.dst, self.device = split, int(dst), device
+        world, me = split.world, split.rank
+        g = group if group is not None else dist.group.WORLD
+        n_z, n_x = split.grid.n_z, split.grid.n_x
+        self.frame = symm.empty((n_z, n_x), dtype=torch.float32, device=device)
+        self.flags = symm.empty((2, world), dtype=torch.int32, device=device)
+        self.flags.zero_()
+        torch.cuda.synchronize(device)
+        self.h_frame = symm.rendezvous(self.frame, g)
+        self.h_flags = symm.rendezvous(self.flags, g)
+        dist.barrier(g)
+        # this rank's rows of the destination's frame, as a tensor the DAS
+        # launch writes (a peer mapping of the destination's memory)
+        self.band = self.h_frame.get_buffer(self.dst, (split.hi - split.lo, n_x), torch.float32,
+                                            split.lo * n_x)
+        self.ready_ptr = self.h_flags.buffer_ptrs[self.dst] + me * 4
+        self.free_ptrs = [p + world * 4 for p in self.h_flags.buffer_ptrs]
+        self.is_dst = me == self.dst
+        self.epoch = 0
+
+    def step(self, plan, rf, range_db: float):
+        """One frame: DAS of this rank's band into the destination's frame;
+        returns (display, status) on dst, None elsewhere."""
+        import torch
+
+        from . import _native as N
+
+        self.epoch += 1
+        e = self.epoch
+        s = N.stream_ptr()
+        with torch.cuda.device(self.device):
+            N.call("bm_wait_flags", self.flags.data_ptr() + self.split.world * 4, 1, e - 1, s)
+            plan.beamform_batch(rf, out=self.band[None])
+            N.call("bm_signal_flag", self.ready_ptr, e, s)
+            if not self.is_dst:
+                return None
+            N.call("bm_wait_flags", self.flags.data_ptr(), self.split.world, e, s)
+            res = envelope_display(self.frame, range_db)
+            for p in self.free_ptrs:
+                N.call("bm_signal_flag", p, e, s)
+        return res
+
+
 def envelope_display(rf_img, range_db: float):
     """Envelope + dB display of one beamformed frame [n_z, n_x] on its device
     (the fused bm_envelope_display of the single-GPU chain).  Returns

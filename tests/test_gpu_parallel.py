@@ -121,5 +121,13 @@ def test_peer_tiles_envelope_kernel_writes_the_gather():
             assert int(status.item()) == 0
             assert torch.equal(disp, full.reconstruct(rf)[0])
         assert peer.epoch == 3
+        # the depth-row split: the DAS kernel stores its band into the
+        # destination's frame buffer
+        rsplit = P.RowSplit(grid, 1, 0)
+        bands = P.PeerBands(rsplit, torch.device("cuda", 0))
+        outs = [tuple(t.clone() for t in bands.step(full.plan, rf, 30.0)) for rf in frames]
+        for rf, (disp, status) in zip(frames, outs):
+            assert int(status.item()) == 0
+            assert torch.equal(disp, full.reconstruct(rf)[0])
     finally:
         dist.destroy_process_group()
