@@ -48,6 +48,7 @@ struct TmaArgs {
   int nst;        // pipeline stages (2 .. kTmaMaxStages)
   int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
   int ls;         // tile shape: lane blocks of (32 >> ls) x (1 << ls) pixels
+  int prefetch;   // with a plan delay table: tiles ahead whose table to prefetch into L2
 };
 
 // shared-memory carve (bytes), identical on host and device
@@ -378,6 +379,19 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
 
   if (producer) {
     // ================= producer warp: window starts + TMA issue
+    if (g.rx_table && a.prefetch > 0 && lane == 0) {
+      // the CTA that will take this one's place on the SM (about `prefetch`
+      // tiles ahead; modulo the grid, so the last wave warms the next
+      // launch's first) finds its delay table in L2
+      const int nt = gridDim.x;
+      const char* nxt = reinterpret_cast<const char*>(g.rx_table) +
+                        (int64_t)((blockIdx.x + a.prefetch) % nt) * n_el * NC * 8;
+      const uint32_t bytes = (uint32_t)n_el * NC * 8;
+      for (uint32_t o = 0; o < bytes; o += 16384)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt + o),
+                     "r"(min(16384u, bytes - o))
+                     : "memory");
+    }
     Cursor cu = c0;
     int s = 0, r = 0;  // stage, round (q = r * nst + s)
     for (int q = 0; q < Q; ++q) {
@@ -782,7 +796,9 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   TmaArgs a{g,   (float*)out, out_stride, n_frames,    e_begin,   e_end,
-            accumulate, fpc,  W,    nst,        tma_cols(g), tma_ls(g)};
+            accumulate, fpc,  W,    nst,        tma_cols(g), tma_ls(g), 0};
+  // tiles between a CTA and its successor on an SM: the co-resident CTAs
+  a.prefetch = debug_override(BM_DBG_DAS_PREFETCH) < 0 ? 0 : (512 / tma_cols(g)) * sm_count();
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
 #define BM_TMA_ROW(J, WT)                                                                  \
