@@ -182,7 +182,7 @@ def cpu_reference(ctx, grid, frames, seconds, interp, max_frames=None):
     """Reference algorithm on the host (oracle/ port): frames/s, threads."""
     from oracle import oracle as O
 
-    plan = O.Plan(ctx, grid, "rectangular", 0.0, np.float32, frames.shape[2])
+    plan = O.Plan(ctx, grid, "rectangular", 0.0, frames.dtype, frames.shape[2])
     O.bmode_chain(frames[0], ctx, grid, interp=interp, plan=plan)  # warm (thread spin-up)
     t0 = time.perf_counter()
     n = 0
@@ -455,7 +455,7 @@ def reference_arm(args, ctx, grid, n_s, world):
     """--impl reference: echopipe itself (baseline/_ref, its own
     pipeline.benchmark on its own SimulatorSource, numba threads = all host
     cores), the C port of the same algorithm timed beside it."""
-    frames = synth_frames(ctx, n_s, 2, 0)
+    frames = synth_frames(ctx, n_s, 2, 0).astype(np.float32 if args.dtype == "f32" else np.float64)
     port = []
     for i in range(args.warmup + args.steps):
         fps, cores, n, el = cpu_reference(ctx, grid, frames, 0.0, args.interp, max_frames=1)
@@ -482,8 +482,9 @@ def reference_arm(args, ctx, grid, n_s, world):
         "impl": "reference", "metric": "B-mode frames/sec", "value": round(val, 4),
         "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic wire phantom + N(0,0.01)",
-        "config": {"workload": WORKLOAD, "frames_per_step": 1},
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic wire phantom + N(0,0.01)",
+        "config": {"workload": WORKLOAD + (", f64" if args.dtype == "f64" else ""),
+                   "frames_per_step": 1},
         "cpu_baseline": {"value": round(val, 4), "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": what},
         "e2e": {"value": round(val, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -533,7 +534,8 @@ def echopipe_benchmark(args, grid_m, n_s, steps, warmup):
                            grid={"x_positions": grid_m.x_positions.tolist(),
                                  "z_positions": grid_m.z_positions.tolist()})
     graph = EPL.build_graph(spec)
-    env = EE.open_simulator(EPR.wire_phantom(), ctx, n_s, dtype=np.float32, seed=0,
+    env = EE.open_simulator(EPR.wire_phantom(), ctx, n_s,
+                            dtype=np.float32 if args.dtype == "f32" else np.float64, seed=0,
                             noise_std=0.01)
     res = EPL.benchmark(graph, env, n_frames=steps, warmup=max(1, warmup))
     n_px = grid_m.n_z * grid_m.n_x
