@@ -150,18 +150,54 @@ def workspace(nbytes: int, device):
     return torch.empty(int(nbytes), dtype=torch.uint8, device=device)
 
 
+_HAVE_CUDA = False
+
+
 def require_cuda():
+    global _HAVE_CUDA
+    if _HAVE_CUDA:
+        return
     import torch
 
     if not torch.cuda.is_available():
         raise NativeError(-2, "no CUDA device: the B200 path has no CPU fallback")
+    _HAVE_CUDA = True
+
+
+class _Same:
+    __slots__ = ()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_SAME = _Same()
+
+
+def on_device(device):
+    """``torch.cuda.device(device)``, or a no-op context when ``device`` is
+    already current (the common case: skips torch's device-index
+    bookkeeping, several microseconds per op)."""
+    import torch
+
+    idx = device.index if isinstance(device, torch.device) else device
+    if idx is None or idx == torch._C._cuda_getDevice():
+        return _SAME
+    return torch.cuda.device(idx)
 
 
 def stream_ptr(stream=None) -> int:
+    """cudaStream_t of `stream`, or of the current stream of the current
+    device (read directly: torch.cuda.current_stream() costs ~10 us of
+    device-index bookkeeping per call, several calls per op)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    return int(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def dtype_code(dtype) -> int:

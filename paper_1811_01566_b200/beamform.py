@@ -134,7 +134,7 @@ class DasPlan:
             setattr(g, name, buf.data_ptr())
         if apod.f_number > 0.0:
             span = torch.empty(2 * grid.n_z * grid.n_x, dtype=torch.int32, device=dev)
-            with torch.cuda.device(dev):
+            with N.on_device(dev):
                 N.call("bm_das_aperture_span", ctypes.byref(g), float(apod.f_number),
                        span.data_ptr(), N.stream_ptr())
             self._bufs["span"] = span
@@ -154,7 +154,7 @@ class DasPlan:
         self.shape = (int(grid.n_z), int(grid.n_x))
         # the geometry uploads and the span kernel ran on the stream current at
         # construction; launches on any other stream wait for this event first
-        with torch.cuda.device(dev):
+        with N.on_device(dev):
             self._ready = torch.cuda.Event()
             self._ready.record()
 
@@ -201,8 +201,9 @@ class DasPlan:
             self._table_refused = True
             return None
         tab = torch.empty(nb // 4, dtype=torch.float32, device=self.device)
-        with torch.cuda.device(self.device):
-            torch.cuda.current_stream().wait_event(self._ready)  # geometry uploaded
+        with N.on_device(self.device):
+            if self._ready is not None:
+                torch.cuda.current_stream().wait_event(self._ready)  # geometry uploaded
             N.call("bm_das_build_table", ctypes.byref(self._geom), tab.data_ptr(), N.stream_ptr())
             ev = torch.cuda.Event()
             ev.record()
@@ -292,8 +293,12 @@ class DasPlan:
             self.delay_table()
         g = self.geometry(n_pad, interp, fast)
         n_img = self.shape[0] * self.shape[1]
-        (stream if stream is not None else torch.cuda.current_stream(self.device)).wait_event(
-            self._ready)
+        if self._ready is not None:
+            if self._ready.query():  # construction copies done: nothing left to order
+                self._ready = None
+            else:
+                (stream if stream is not None else torch.cuda.current_stream(self.device)
+                 ).wait_event(self._ready)
         e0, e1 = tx_range if tx_range is not None else (0, n_tx)
         for f0 in range(0, f, 65535):
             nf = min(65535, f - f0)

@@ -72,7 +72,7 @@ def _fir_device(x, spec: FirSpec, axis: int, out_dtype):
         taps = torch.from_numpy(np.array(spec.coefficients, dtype=np.float64)).to(x.device)
         code_in = N.BM_F32 if x.dtype == torch.float32 else N.BM_F64
         code_out = N.BM_F32 if out_dtype == torch.float32 else N.BM_F64
-        with torch.cuda.device(x.device):
+        with N.on_device(x.device):
             N.call("bm_fir_filter", code_in, x.data_ptr(), code_out, y.data_ptr(), outer, n, inner,
                    taps.data_ptr(), int(taps.numel()), N.stream_ptr())
     return y
@@ -133,7 +133,7 @@ def analytic_signal(x, axis: int = -1):
     z = torch.empty(shape + (2,), dtype=tdt, device=dev)
     if xd.numel():
         code = N.dtype_code(rdt)
-        with torch.cuda.device(dev):
+        with N.on_device(dev):
             nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ANALYTIC, code, outer, n, inner))
             ws = N.workspace(nb, dev)
             N.call("bm_analytic_signal", code, xd.data_ptr(), z.data_ptr(), outer, n, inner,
@@ -160,7 +160,7 @@ def envelope(z):
         zd = zd.to(torch.complex128)
     zr = torch.view_as_real(zd.contiguous())
     e = torch.empty(zd.shape, dtype=rdt, device=dev)
-    with torch.cuda.device(dev):
+    with N.on_device(dev):
         N.call("bm_envelope", N.BM_F32 if rdt == torch.float32 else N.BM_F64, zr.data_ptr(),
                e.data_ptr(), zd.numel(), N.stream_ptr())
     return e if is_t and z.is_cuda else e.cpu().numpy()
@@ -178,7 +178,7 @@ def _abs_device(x, is_t):
     xd = to_device(x, dev, tdt)
     e = torch.empty_like(xd)
     if xd.numel():
-        with torch.cuda.device(dev):
+        with N.on_device(dev):
             N.call("bm_abs", N.dtype_code(dt), xd.data_ptr(), e.data_ptr(), xd.numel(),
                    N.stream_ptr())
     return e if is_t and x.is_cuda else e.cpu().numpy()
@@ -193,7 +193,7 @@ def envelope_peak_device(x, n_frames: int, n_z: int, n_x: int):
     env = torch.empty_like(x)
     peak = torch.empty(n_frames, dtype=torch.int32 if code == N.BM_F32 else torch.int64,
                        device=x.device)
-    with torch.cuda.device(x.device):
+    with N.on_device(x.device):
         nb = int(N.load().bm_sigproc_ws_bytes(N.SIG_ENVELOPE_PEAK, code, n_frames, n_z, n_x))
         ws = N.workspace(nb, x.device)
         N.call("bm_envelope_peak", code, x.data_ptr(), env.data_ptr(), peak.data_ptr(), n_frames,
@@ -209,7 +209,7 @@ def _dyn_device(e, range_db: float, peak=None):
     code = N.BM_F32 if e.dtype == torch.float32 else N.BM_F64
     disp = torch.empty_like(e)
     status = torch.empty(1, dtype=torch.int32, device=dev)
-    with torch.cuda.device(dev):
+    with N.on_device(dev):
         if peak is None:
             peak = torch.empty(1, dtype=torch.int32 if code == N.BM_F32 else torch.int64, device=dev)
             N.call("bm_dynamic_adjustment", code, e.data_ptr(), peak.data_ptr(), disp.data_ptr(),
