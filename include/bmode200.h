@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BMODE200_ABI_VERSION 3
+#define BMODE200_ABI_VERSION 4
 
 /* element type of every floating-point buffer of one call */
 enum { BM_F32 = 0, BM_F64 = 1 };
@@ -114,6 +114,13 @@ typedef struct bm_das_geometry {
   const float* rx_table;     /* optional DEVICE table from bm_das_build_table: the
                                 receive delays of every tile, read instead of being
                                 rebuilt by each CTA (same bits); NULL = rebuild */
+  const uint32_t* tx_ready;  /* optional DEVICE counter for a launch that starts while
+                                its frame is still being copied in: the launch reads
+                                transmit e's RF only after the counter has reached
+                                tx_ready_base + e + 1 (compared modulo 2^32), the
+                                copy side advancing it behind each landed transmit
+                                group with bm_stream_write_u32.  NULL = RF resident */
+  uint32_t tx_ready_base;
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64
@@ -251,6 +258,30 @@ int bm_check_finite(int32_t dtype, const void* x, int64_t count, int32_t* flag, 
  * (system-scope acquire).  One tiny kernel each. */
 int bm_signal_flag(int32_t* flag, int32_t value, void* stream);
 int bm_wait_flags(const int32_t* flags, int32_t n, int32_t value, void* stream);
+
+/* Stream-ordered 32-bit store *addr = value (device memory) performed by the
+ * stream's front end once every earlier operation of `stream` -- copies
+ * included -- has completed and is visible (cuStreamWriteValue32 with its
+ * default memory barrier).  It needs no SM, so it can release a kernel that
+ * is already running on another stream and waits on *addr: the RF copy of a
+ * host frame advances g->tx_ready with it behind each transmit group while
+ * the DAS launch beamforms the groups that have landed. */
+int bm_stream_write_u32(uint32_t* addr, uint32_t value, void* stream);
+
+/* Upload of one HOST frame (the RF ingest in front of
+ * das_beamform): copies `src` (pageable host memory) into the caller's pinned
+ * `staging` buffer and on to the device buffer `dst`, in n_pieces pieces
+ * (piece k = bytes [ends[k-1], ends[k]), ends[-1] = 0).  Each piece is
+ * copied by the library's host threads (up to 8) with non-temporal stores,
+ * so the DMA that follows reads DRAM rather than CPU-dirty cache lines;
+ * then its DMA staging -> dst is enqueued on `stream` and, when `counter` is
+ * non-NULL, the store *counter = values[k] (bm_stream_write_u32) -- the
+ * progress a DAS launch with g->tx_ready waits on.  The DMA of piece k
+ * overlaps the host copy of piece k + 1.  Returns once every piece is
+ * enqueued; `staging` must stay untouched until `stream` passes the last
+ * DMA.  Calls from several host threads are serialised. */
+int bm_host_upload(void* dst, const void* src, void* staging, const int64_t* ends,
+                   int32_t n_pieces, uint32_t* counter, const uint32_t* values, void* stream);
 
 /* dynamic_adjustment as one call: bm_frame_peak then bm_display. */
 int bm_dynamic_adjustment(int32_t dtype, const void* e, void* peak_ws, void* disp,

@@ -19,53 +19,36 @@ _stage = threading.local()
 
 
 def _staged_h2d(src, device):
-    """Copy a contiguous CPU tensor to ``device`` through one of two per-thread
-    pinned buffers; the copy is enqueued on the current stream."""
+    """Copy a contiguous CPU tensor to ``device`` through the per-thread
+    pinned staging buffers; the copy is enqueued on the current stream."""
     import torch
 
-    pool = getattr(_stage, "pool", None)
-    if pool is None:
-        pool = _stage.pool = {"bufs": [None, None], "events": [None, None], "next": 0}
-    i = pool["next"]
-    pool["next"] ^= 1
-    nbytes = src.numel() * src.element_size()
-    buf = pool["bufs"][i]
-    if buf is None or buf.numel() < nbytes:
-        buf = pool["bufs"][i] = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),
-                                            dtype=torch.uint8, pin_memory=True)
-        pool["events"][i] = None
-    ev = pool["events"][i]
-    if ev is not None:
-        ev.synchronize()  # the DMA that last read this buffer has finished
-    stage = buf[:nbytes].view(src.dtype)
-    flat = src.reshape(-1)
     out = torch.empty(src.shape, dtype=src.dtype, device=device)
-    oflat = out.view(-1)
-    # chunked: the DMA of chunk i overlaps the host memcpy of chunk i + 1
-    n = flat.numel()
-    step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
-    with torch.cuda.device(device):
-        for o in range(0, n, step):
-            stage[o:o + step].copy_(flat[o:o + step])
-            oflat[o:o + step].copy_(stage[o:o + step], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-    pool["events"][i] = ev
+    staged_copy_into(src, out, torch.cuda.current_stream(device))
     return out
 
 
-def staged_copy_into(src, dst, stream):
+def staged_copy_into(src, dst, stream, splits=None, counter=None, values=None):
     """Copy a contiguous CPU tensor into the device tensor ``dst`` (same
-    numel) through the per-thread pinned staging buffers, enqueued on
-    ``stream``; returns the event that follows the last DMA."""
+    numel) through one of two per-thread pinned staging buffers, enqueued on
+    ``stream`` by bm_host_upload (multi-threaded streaming-store host copy,
+    then the DMA, piece by piece); returns the event that follows the last
+    DMA.  ``splits``: increasing end offsets (elements) of the pieces, else
+    four for >= 4 MB.  ``counter``/``values``: device uint32 progress word
+    and the value stored behind each piece (bm_stream_write_u32)."""
+    import ctypes
+
     import torch
+
+    from . import _native as N
 
     pool = getattr(_stage, "pool", None)
     if pool is None:
         pool = _stage.pool = {"bufs": [None, None], "events": [None, None], "next": 0}
     i = pool["next"]
     pool["next"] ^= 1
-    nbytes = src.numel() * src.element_size()
+    esz = src.element_size()
+    nbytes = src.numel() * esz
     buf = pool["bufs"][i]
     if buf is None or buf.numel() < nbytes:
         buf = pool["bufs"][i] = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),
@@ -74,17 +57,18 @@ def staged_copy_into(src, dst, stream):
     ev = pool["events"][i]
     if ev is not None:
         ev.synchronize()  # the DMA that last read this buffer has finished
-    stage = buf[:nbytes].view(src.dtype)
-    flat, oflat = src.reshape(-1), dst.view(-1)
-    # in pieces: the DMA of one overlaps the host memcpy of the next
-    n = flat.numel()
-    step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
-    with torch.cuda.stream(stream):
-        for o in range(0, n, step):
-            stage[o:o + step].copy_(flat[o:o + step])
-            oflat[o:o + step].copy_(stage[o:o + step], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(stream)
+    n = src.numel()
+    if splits is None:
+        step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
+        splits = list(range(step, n, step)) + [n]
+    k = len(splits)
+    ends = (ctypes.c_int64 * k)(*[int(e) * esz for e in splits])
+    vals = (ctypes.c_uint32 * k)(*[int(v) & 0xFFFFFFFF for v in values]) if counter else None
+    src = src.contiguous()
+    N.call("bm_host_upload", dst.data_ptr(), src.data_ptr(), buf.data_ptr(), ends, k,
+           counter, vals, int(stream.cuda_stream))
+    ev = torch.cuda.Event()
+    ev.record(stream)
     pool["events"][i] = ev
     return ev
 

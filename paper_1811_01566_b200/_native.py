@@ -20,7 +20,7 @@ BM_STA, BM_PW = 0, 1
 BM_NEAREST, BM_LINEAR = 0, 1
 BM_RECTANGULAR, BM_HANN = 0, 1
 BM_ERR_AXIS_TOO_SHORT = 4
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # bm_sigproc_ws_bytes ops
 SIG_ANALYTIC, SIG_ENVELOPE_PEAK, SIG_ENVELOPE_DISPLAY = 0, 1, 2
@@ -48,7 +48,8 @@ class DasGeometry(ctypes.Structure):
         ("tx_elements", ctypes.c_void_p), ("cos_a", ctypes.c_void_p), ("sin_a", ctypes.c_void_p),
         ("rx_map", ctypes.c_void_p), ("t0_smp", ctypes.c_void_p), ("hann", ctypes.c_void_p),
         ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32), ("tile_ls", ctypes.c_int32),
-        ("rx_table", ctypes.c_void_p),
+        ("rx_table", ctypes.c_void_p), ("tx_ready", ctypes.c_void_p),
+        ("tx_ready_base", ctypes.c_uint32),
     ]
 
 
@@ -82,6 +83,8 @@ SIGNATURES = {
     "bm_display_tiles": ([_I32, _P, _I32, _I64, _I64, _I64, _P, _P, _D, _P], ctypes.c_int),
     "bm_check_finite": ([_I32, _P, _I64, _P, _P], ctypes.c_int),
     "bm_signal_flag": ([_P, _I32, _P], ctypes.c_int),
+    "bm_stream_write_u32": ([_P, ctypes.c_uint32, _P], ctypes.c_int),
+    "bm_host_upload": ([_P, _P, _P, _P, _I32, _P, _P, _P], ctypes.c_int),
     "bm_wait_flags": ([_P, _I32, _I32, _P], ctypes.c_int),
     "bm_frame_peak": ([_I32, _P, _P, _I32, _I64, _P], ctypes.c_int),
     "bm_display": ([_I32, _P, _P, _P, _P, _I32, _I64, _D, _P], ctypes.c_int),

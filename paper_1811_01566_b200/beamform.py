@@ -24,6 +24,7 @@ libbmode200.so; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -168,21 +169,20 @@ class DasPlan:
     # launch, when it fits this share of the free device memory
     TABLE_MAX_FRAMES = 2
     TABLE_MEM_SHARE = 0.25
-    # a host frame's copy can be split into transmit chunks whose DAS overlaps
-    # the next chunk's copy (beamform_host); measured on cfg2, every launch
-    # pays its CTAs' setup (delay-table read, TMEM, pipeline fill) again, so
-    # 2 / 3 / 4 chunks gave 974 / 852 / 941 drop-in frames/s against 1 048
-    # for one: one chunk by default (tools/dropin_chunks.sh)
-    HOST_CHUNKS = 1
+    # a host frame's copy travels in this many transmit groups, the one DAS
+    # launch reading each group as it lands (beamform_host)
+    HOST_PIECES = 4
+
+    @property
+    def torch_dtype(self):
+        import torch
+
+        return torch.float32 if self.dtype == np.float32 else torch.float64
 
     def host_overlap_ok(self, n_samples: int) -> bool:
-        """beamform_host applies: f32 frames on the TMA kernel with 16-B rows."""
-        ok = getattr(self, "_host_ok", {})
-        if n_samples not in ok:
-            ok[n_samples] = (self.dtype == np.float32 and int(n_samples) % 4 == 0
-                             and self.kernel_for(n_samples) == "tma-ws")
-            self._host_ok = ok
-        return ok[n_samples]
+        """beamform_host applies: trace rows already 16-B aligned (no padding
+        copy, which would read the frame before it lands)."""
+        return self._padded(n_samples, True) == int(n_samples)
 
     def delay_table(self, build: bool = True):
         """The plan's device receive-delay table (the role of the reference
@@ -254,11 +254,15 @@ class DasPlan:
                          "window"), list(shape)))
 
     def beamform_batch(self, rf, interp: str = "linear", out=None, stream=None, fast=True,
-                       tx_range=None, accumulate=False):
+                       tx_range=None, accumulate=False, tx_ready=None):
         """DAS of a device batch ``rf [F, n_tx, n_rx, n_s]`` (or one frame
         ``[n_tx, n_rx, n_s]``) into ``out [F, n_z, n_x]`` on ``stream``.
         ``tx_range=(e0, e1)`` beamforms those transmits only; ``accumulate``
-        continues the sums already in ``out`` (bm_das_beamform_range)."""
+        continues the sums already in ``out`` (bm_das_beamform_range).
+        ``tx_ready=(counter_ptr, base)``: ``rf`` is still being copied in on
+        another stream, which advances the device counter behind each landed
+        transmit group (g.tx_ready, bm_stream_write_u32); the launch reads
+        transmit e once the counter reaches base + e + 1."""
         import torch
 
         if interp not in INTERPOLATION_MODES:
@@ -276,6 +280,8 @@ class DasPlan:
             out = torch.empty((f,) + self.shape, dtype=rfb.dtype, device=self.device)
         n_pad = n_s
         if fast and (n_s != self._padded(n_s, True) or not rfb.is_contiguous()):
+            if tx_ready is not None:  # the padding copy would read RF still in flight
+                raise ValueError("tx_ready launches need contiguous, 16-B aligned trace rows")
             # the TMA kernels want 16-B trace rows: copy into rows of a multiple
             # of 4 (f32) / 2 (f64) samples, zero tail (bm_pad_traces; bitwise
             # the same result)
@@ -292,6 +298,8 @@ class DasPlan:
         if fast and f <= self.TABLE_MAX_FRAMES:
             self.delay_table()
         g = self.geometry(n_pad, interp, fast)
+        if tx_ready is not None:
+            g.tx_ready, g.tx_ready_base = int(tx_ready[0]), int(tx_ready[1]) & 0xFFFFFFFF
         n_img = self.shape[0] * self.shape[1]
         if self._ready is not None:
             if self._ready.query():  # construction copies done: nothing left to order
@@ -318,38 +326,60 @@ def _tx_chunks(n_tx: int, k: int):
         lo = hi
 
 
-def beamform_host(plan: DasPlan, data, interp: str = "linear", chunks: int | None = None):
+_host_copy = threading.local()
+
+
+def _copy_state(dev):
+    """Per (thread, device): the copy stream host frames travel on and the
+    device counter (uint32) its bm_stream_write_u32 stores advance.  One
+    thread's calls are sequential and each call's copies start after the
+    previous call's launch (wait_stream), so its counter only moves forward."""
+    import torch
+
+    by_dev = getattr(_host_copy, "by_dev", None)
+    if by_dev is None:
+        by_dev = _host_copy.by_dev = {}
+    st = by_dev.get(dev.index)
+    if st is None:
+        st = by_dev[dev.index] = {"stream": torch.cuda.Stream(dev),
+                                  "counter": torch.zeros(1, dtype=torch.int32, device=dev),
+                                  "base": 0}
+    return st
+
+
+def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | None = None):
     """One HOST frame (numpy, [n_tx, n_rx, n_s]) -> device rf image, the
-    host->device copy of transmit chunk k+1 overlapping the DAS of chunk k:
-    chunk k's copy runs on a copy stream, its beamforming launch
-    (bm_das_beamform_range) waits for that copy only and continues the sums
-    of chunks < k -- so the bits equal one launch over the whole frame."""
+    frame's host->device copy overlapping its own Delay-and-Sum (SURVEY
+    8(f) #1): the copy runs on a copy stream in ``pieces`` transmit groups,
+    each followed by a stream-ordered store of the landed-transmit count
+    (bm_stream_write_u32), and ONE launch -- issued once every piece is
+    enqueued, so no exception can strand it -- reads transmit e as soon as
+    the count passes it (g.tx_ready).  The launch is the same kernel over
+    the same data, so the bits equal a launch on the resident frame."""
     import torch
 
     from ._device import staged_copy_into
 
     data = np.ascontiguousarray(data)
     n_tx, n_rx, n_s = data.shape
-    if chunks is None:
-        chunks = plan.HOST_CHUNKS
-    chunks = max(1, min(int(chunks), n_tx))
+    pieces = max(1, min(int(pieces or plan.HOST_PIECES), n_tx))
     dev = plan.device
-    copy_stream = getattr(plan, "_copy_stream", None)
-    if copy_stream is None:
-        copy_stream = plan._copy_stream = torch.cuda.Stream(dev)
-    comp = torch.cuda.current_stream(dev)
+    st = _copy_state(dev)
+    cs, comp = st["stream"], torch.cuda.current_stream(dev)
     # a buffer per call (plans are shared between threads); the copy stream
-    # writes it only after the allocating stream's earlier work, and every
-    # launch that reads it waits for its copies
-    rf = torch.empty((1, n_tx, n_rx, n_s), dtype=torch.float32, device=dev)
-    copy_stream.wait_stream(comp)
-    src = torch.from_numpy(data)
-    out = torch.empty((1,) + plan.shape, dtype=torch.float32, device=dev)
-    for k, (e0, e1) in enumerate(_tx_chunks(n_tx, chunks)):
-        ev = staged_copy_into(src[e0:e1], rf[0, e0:e1], copy_stream)
-        comp.wait_event(ev)
-        plan.beamform_batch(rf, interp, out=out, stream=comp, tx_range=(e0, e1),
-                            accumulate=k > 0)
+    # writes it only after the allocating stream's earlier work
+    rf = torch.empty((1, n_tx, n_rx, n_s), dtype=plan.torch_dtype, device=dev)
+    out = torch.empty((1,) + plan.shape, dtype=plan.torch_dtype, device=dev)
+    cs.wait_stream(comp)
+    base = st["base"]
+    st["base"] = (base + n_tx) & 0xFFFFFFFF
+    ctr = st["counter"].data_ptr()
+    bounds = list(_tx_chunks(n_tx, pieces))
+    done = staged_copy_into(torch.from_numpy(data), rf, cs,
+                            splits=[e1 * n_rx * n_s for _, e1 in bounds], counter=ctr,
+                            values=[base + e1 for _, e1 in bounds])
+    plan.beamform_batch(rf, interp, out=out, stream=comp, tx_ready=(ctr, base))
+    comp.wait_event(done)  # later users of rf on comp (its reuse) follow the copy
     return out[0]
 
 

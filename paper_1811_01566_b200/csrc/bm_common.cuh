@@ -56,6 +56,31 @@ inline int sm_count() {
   return n;
 }
 
+// Transmits of the launch's frame that have landed in device memory, for a
+// launch started while its RF is still being copied in (g.tx_ready; the copy
+// side advances the counter with bm_stream_write_u32): waits until the
+// counter has passed base + need (modulo 2^32) and returns how many
+// transmits are then known present.  The acquire orders this thread's later
+// RF reads after the copies; a TMA issuer adds fence.proxy.async.  A counter
+// that never arrives (a host-side bug) traps after ~10 s instead of leaving
+// the device hung.
+__device__ __forceinline__ int wait_tx_ready(const uint32_t* ctr, uint32_t base, int need) {
+  uint64_t t_first = 0;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    const int have = (int)(v - base);
+    if (have >= need) return have;
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t_first == 0)
+      t_first = now;
+    else if (now - t_first > 10000000000ull)
+      __trap();
+    __nanosleep(200);
+  }
+}
+
 // TMA DAS kernel (bm_das_tma.cu)
 int das_tma_eligible(const bm_das_geometry& g, int64_t rf_stride);
 int das_tma_shape(const bm_das_geometry& g, int n_frames, int32_t* shape);

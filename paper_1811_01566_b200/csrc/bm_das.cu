@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(TZ * kTileX) das_kernel(const DasArgs a) {
   const T* __restrict__ t0s = reinterpret_cast<const T*>(g.t0_smp);
   T* __restrict__ outp = reinterpret_cast<T*>(a.out) + (int64_t)blockIdx.y * a.out_stride + p;
   T acc = a.accumulate && valid ? *outp : T(0);
+  if (g.tx_ready) {  // RF still being copied in: start once the launch's transmits landed
+    if (tid == 0) wait_tx_ready(g.tx_ready, g.tx_ready_base, a.e_end);
+    __syncthreads();
+  }
   for (int e = a.e_begin; e < a.e_end; ++e) {
     T txd;
     if (PW) {

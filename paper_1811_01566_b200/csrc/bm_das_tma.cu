@@ -394,10 +394,15 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
     }
     Cursor cu = c0;
     int s = 0, r = 0;  // stage, round (q = r * nst + s)
+    int landed = 0;    // transmits known copied in (g.tx_ready launches)
     for (int q = 0; q < Q; ++q) {
       // round r >= 1 reuses stage s: wait for the consumers' release of round r-1
       if (r > 0) mbar_wait_sleep(empty_s + 8 * s, (uint32_t)(r - 1) & 1u);
       const int e = cu.e;
+      if (g.tx_ready && e >= landed) {  // this transmit's RF may still be in flight
+        landed = wait_tx_ready(g.tx_ready, g.tx_ready_base, e + 1);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
+      }
       const float t0 = t0v[e];
       const float lo_e = tmin[e] - t0;
       const int jb = cu.cb * TJC;

@@ -294,9 +294,14 @@ __global__ void __launch_bounds__(288, 1)
   if (producer) {
     Cursor cu = c0;
     int s = 0, r = 0;
+    int landed = 0;  // transmits known copied in (g.tx_ready launches)
     for (int q = 0; q < Q; ++q) {
       if (r > 0) mbar_wait_sleep(empty_s + 8 * s, (uint32_t)(r - 1) & 1u);
       const int e = cu.e;
+      if (g.tx_ready && e >= landed) {
+        landed = wait_tx_ready(g.tx_ready, g.tx_ready_base, e + 1);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       const float lo_e = tmin[e] - (float)t0v[e];
       const int jb = cu.cb * kJ64, jn = min(kJ64, n_rx - jb);
       const int ngr = (jn + G - 1) / G;

@@ -26,7 +26,10 @@
 // computes its next item before it waits for the previous one's frame, so
 // every wait is on a frame whose items were all dealt out and are computed
 // without waiting (no deadlock).
+#include <cuda.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "bm_fft.cuh"
 
@@ -1216,6 +1219,28 @@ extern "C" int bm_wait_flags(const int32_t* flags, int32_t n, int32_t value, voi
   if (!flags || n < 1) return BM_ERR_INVALID_ARGUMENT;
   wait_flags_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flags, n, value);
   return cuda_status();
+}
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+extern "C" int bm_stream_write_u32(uint32_t* addr, uint32_t value, void* stream) {
+  static StreamWriteValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWriteValue32Fn>(p);
+    else
+      cudaGetLastError();
+  });
+  if (!addr || (reinterpret_cast<uintptr_t>(addr) & 3)) return BM_ERR_INVALID_ARGUMENT;
+  if (!fn) return BM_ERR_UNSUPPORTED;
+  // flags 0 = CU_STREAM_WRITE_VALUE_DEFAULT: a memory barrier precedes the write
+  return fn((CUstream)stream, (CUdeviceptr)addr, value, 0) == CUDA_SUCCESS ? BM_OK : BM_ERR_CUDA;
 }
 
 extern "C" int bm_frame_peak(int32_t dtype, const void* e, void* peak, int32_t n_frames,

@@ -121,6 +121,39 @@ def test_staged_host_to_device_copies_are_exact_and_do_not_alias():
     assert f64.dtype == torch.float64 and torch.equal(f64.cpu(), torch.from_numpy(hosts[1].astype(np.float64)))
 
 
+def test_host_upload_pieces_counter_and_odd_sizes():
+    """bm_host_upload: byte-exact for odd sizes and unaligned source /
+    destination offsets, empty pieces allowed, the counter ends at the last
+    piece's value; bad arguments rejected before any work."""
+    import ctypes
+
+    import torch
+
+    from paper_1811_01566_b200 import _native as N
+
+    rng = np.random.default_rng(9)
+    lib = N.load()
+    st = torch.cuda.current_stream()
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for nbytes, cuts in ((1, [1]), (1000, [0, 999, 1000]), (3 << 20, [1 << 20, 1 << 20, 3 << 20]),
+                         ((5 << 20) + 13, [7, (2 << 20) + 1, (5 << 20) + 13])):
+        src = rng.integers(0, 256, size=nbytes + 3, dtype=np.uint8)
+        stage = torch.empty(nbytes + 64, dtype=torch.uint8, pin_memory=True)
+        dst = torch.zeros(nbytes + 5, dtype=torch.uint8, device="cuda")
+        ends = (ctypes.c_int64 * len(cuts))(*cuts)
+        vals = (ctypes.c_uint32 * len(cuts))(*[100 + i for i in range(len(cuts))])
+        # odd offsets: source +3, staging +1, destination +5
+        N.call("bm_host_upload", dst.data_ptr() + 5, src.ctypes.data + 3, stage.data_ptr() + 1,
+               ends, len(cuts), counter.data_ptr(), vals, st.cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(dst[5:].cpu().numpy(), src[3:]), nbytes
+        assert int(counter.item()) == 100 + len(cuts) - 1
+    bad = (ctypes.c_int64 * 2)(8, 4)  # decreasing ends
+    assert lib.bm_host_upload(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src.ctypes.data),
+                              ctypes.c_void_p(stage.data_ptr()), bad, 2, None, None,
+                              ctypes.c_void_p(st.cuda_stream)) == 1
+
+
 def test_device_frame_finiteness_scan_on_the_gpu():
     """RfFrame of a CUDA tensor runs the reference's finiteness check
     (types.py:41-42) with bm_check_finite: NaN and inf rejected."""

@@ -33,7 +33,7 @@ def test_library_built_for_sm100a_and_exports_header_symbols():
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES), "ctypes signatures out of sync with the header"
     lib.bm_abi_version.restype = ctypes.c_int
-    assert lib.bm_abi_version() == 3
+    assert lib.bm_abi_version() == 4
     lib.bm_error_string.restype = ctypes.c_char_p
     assert lib.bm_error_string(4) == b"analytic signal needs axis length >= 2"
 
@@ -51,7 +51,32 @@ def test_geometry_struct_layout():
     assert N.DasGeometry.rx_contig.offset == 16 * 4 + 2 * 8 + 10 * 8
     assert N.DasGeometry.tile_ls.offset == 16 * 4 + 2 * 8 + 10 * 8 + 4
     assert N.DasGeometry.rx_table.offset == 16 * 4 + 2 * 8 + 10 * 8 + 8
-    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 8 + 8
+    assert N.DasGeometry.tx_ready.offset == 16 * 4 + 2 * 8 + 10 * 8 + 16
+    assert N.DasGeometry.tx_ready_base.offset == 16 * 4 + 2 * 8 + 10 * 8 + 24
+    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 32
+
+
+def test_geometry_struct_matches_c_compiler(tmp_path):
+    """offsetof / sizeof of bm_das_geometry as gcc lays it out == the ctypes mirror."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    fields = [f for f, _ in N.DasGeometry._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"bmode200.h\"\n"
+                   "int main(void) {\n" +
+                   "".join(f'  printf("%zu\\n", offsetof(bm_das_geometry, {f}));\n'
+                           for f in fields) +
+                   '  printf("%zu\\n", sizeof(bm_das_geometry));\n  return 0;\n}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [getattr(N.DasGeometry, f).offset for f in fields] + [ctypes.sizeof(N.DasGeometry)]
+    assert got == want
 
 
 def test_invalid_arguments_rejected_without_gpu():
