@@ -343,7 +343,10 @@ enum {
   BM_DBG_NO_FUSED_DISPLAY = 10,/* bm_envelope_display: envelope + display launches  */
   BM_DBG_FIR_ONE_OUTPUT = 11,  /* FIR: one output per thread kernel                  */
   BM_DBG_DAS_PREFETCH = 12,    /* TMA: -1 = no L2 prefetch of the next tiles' tables */
-  BM_DBG_COUNT = 13
+  BM_DBG_DAS_LATE_PRODUCER = 13, /* TMA: 1 = the producer waits for the delay table
+                                    (pre-v4 order; default: it fills the RF stages
+                                    while the consumers build their delays)         */
+  BM_DBG_COUNT = 14
 };
 int bm_debug_set(int32_t key, int32_t value); /* returns the previous value     */
 int bm_debug_get(int32_t key);

@@ -29,7 +29,7 @@ SIG_ANALYTIC, SIG_ENVELOPE_PEAK, SIG_ENVELOPE_DISPLAY = 0, 1, 2
 DEBUG_KEYS = {"das_kernel": 0, "das_fp": 1, "das_ft": 2, "das_fpc": 3, "das_tjc": 4,
               "das_runtime_w": 5, "das_tile": 6, "das_verbose": 7, "das_generic_tz": 8,
               "fft_path": 9, "no_fused_display": 10, "fir_one_output": 11,
-              "das_prefetch": 12}
+              "das_prefetch": 12, "das_late_producer": 13}
 
 
 class DasGeometry(ctypes.Structure):

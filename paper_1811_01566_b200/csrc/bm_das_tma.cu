@@ -49,6 +49,7 @@ struct TmaArgs {
   int tmem_cols;  // allocated TMEM columns (power of two >= 2 * n_elements)
   int ls;         // tile shape: lane blocks of (32 >> ls) x (1 << ls) pixels
   int prefetch;   // with a plan delay table: tiles ahead whose table to prefetch into L2
+  int early_producer;  // 1: the RF pipeline fills while the consumers build their delays
 };
 
 // shared-memory carve (bytes), identical on host and device
@@ -207,11 +208,14 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   // WT: the pair's active element spans (all elements without an F-number)
   int i0A = 0, i1A = n_el - 1, i0B = 0, i1B = n_el - 1;
   // ---- exact receive delays of the consumer thread's pixel pair -> TMEM
-  if (!producer) {
+  auto load_delays = [&]() {
     if (g.rx_table) {
       // precomputed per plan (bm_das_build_table, the same bits): 32 loads
       // in flight per thread (a CTA's 128 KB arrives at ~HBM latency x 4, not
-      // x 16), streamed past L2 (the RF windows want it)
+      // x 16), streamed past L2 (the RF windows want it).  Evaluating part of
+      // the elements while the loads fly instead was slower at every split
+      // tried (cfg2 one frame: 2/16 of the elements 0.177 ms, 8/16 0.211,
+      // against 0.165 ms reading them all)
       const float2* tb =
           reinterpret_cast<const float2*>(g.rx_table) + (int64_t)blockIdx.x * n_el * NC + ctid;
       int m = slot;
@@ -257,8 +261,25 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
         whi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi + 1)) - 1;
       }
     }
+    if (PW && slot == 0) {
+      // exact transmit delays fs*((z cos + x sin)/c) of the pixel pair for every
+      // angle (beamform.py:218-225), once per CTA
+      for (int e = 0; e < n_tx; ++e) {
+        const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
+        const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
+        const float xs = O::mul(pxd, sa);
+        const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
+        const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
+        txd_s[e * NC + ctid] = pk(tA, tB);
+      }
+    }
     tm_wait_st();
-  }
+  };
+  // SKIP needs every warp's span before the stage ranges exist; otherwise the
+  // producer starts filling the RF pipeline while the consumers build their
+  // delays (the consumers then meet at a barrier of their own)
+  const bool early = !SKIP && a.early_producer;
+  if (!producer && !early) load_delays();
 
   const int zl = min(tz0 + TZk, g.n_z) - 1;
   const double x0 = g.x_pos[tx0], x1 = g.x_pos[min(tx0 + TXk, g.n_x) - 1];
@@ -290,19 +311,17 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
       rx_bounds(g.tx_elements[e], tmin[e], tmax[e]);
     }
   }
-  if (PW && !producer && slot == 0) {
-    // exact transmit delays fs*((z cos + x sin)/c) of the pixel pair for every
-    // angle (beamform.py:218-225), once per CTA
-    for (int e = 0; e < n_tx; ++e) {
-      const float ca = reinterpret_cast<const float*>(g.cos_a)[e];
-      const float sa = reinterpret_cast<const float*>(g.sin_a)[e];
-      const float xs = O::mul(pxd, sa);
-      const float tA = O::mul(fs, O::div(O::add(O::mul(pzA, ca), xs), c));
-      const float tB = O::mul(fs, O::div(O::add(O::mul(pzB, ca), xs), c));
-      txd_s[e * NC + ctid] = pk(tA, tB);
-    }
-  }
+  tm_fence_before();
   __syncthreads();
+  tm_fence_after();
+  if (!producer && early) {
+    load_delays();
+    // the consumers' own barrier: TMEM columns and transmit delays written by
+    // the other warps of the lane quarter / of slot 0
+    tm_fence_before();
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * NCW) : "memory");
+    tm_fence_after();
+  }
 
   // WT: the Hann rows (beamform.py:48-63) are read through L1 from the
   // plan's table: the element row without an F-number (one row for every
@@ -804,6 +823,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
             accumulate, fpc,  W,    nst,        tma_cols(g), tma_ls(g), 0};
   // tiles between a CTA and its successor on an SM: the co-resident CTAs
   a.prefetch = debug_override(BM_DBG_DAS_PREFETCH) < 0 ? 0 : (512 / tma_cols(g)) * sm_count();
+  a.early_producer = debug_override(BM_DBG_DAS_LATE_PRODUCER) == 1 ? 0 : 1;
   const bool pw = g.scheme == BM_PW, lin = g.interp == BM_LINEAR;
   typedef void (*kfn)(const CUtensorMap, const TmaArgs);
 #define BM_TMA_ROW(J, WT)                                                                  \

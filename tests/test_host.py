@@ -56,6 +56,13 @@ def test_geometry_struct_layout():
     assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 32
 
 
+def test_debug_keys_match_header_enum():
+    src = open(os.path.join(ROOT, "include", "bmode200.h")).read()
+    enum = {k.lower(): int(v) for k, v in re.findall(r"BM_DBG_(\w+) = (\d+)", src)}
+    count = enum.pop("count")
+    assert enum == N.DEBUG_KEYS and count == len(enum)
+
+
 def test_geometry_struct_matches_c_compiler(tmp_path):
     """offsetof / sizeof of bm_das_geometry as gcc lays it out == the ctypes mirror."""
     import shutil
