@@ -170,3 +170,34 @@ def test_device_frame_finiteness_scan_on_the_gpu():
             bm.RfFrame(y)
         with pytest.raises(InvalidMetadata):
             bm.RfFrame(y.double())
+
+
+def test_stage_times_bracket_each_ops_gpu_work():
+    """execute's CUDA-event stage times hold each node's own GPU work: the
+    beamform stage of the sta-paper preset is at least most of the same op
+    timed alone (an event on the wrong stream would leave the DAS outside
+    it and charge it to a later stage)."""
+    import statistics
+
+    import torch
+
+    from paper_1811_01566_b200 import cli
+    from paper_1811_01566_b200.pipeline import _to_device_obs
+
+    env = cli.preset_environment("sta-paper")
+    g = bm.build_graph(cli.preset_pipeline("sta-paper"))
+    obs = _to_device_obs(env.next_observation())
+    for _ in range(3):
+        bm.execute(g, obs)
+    stage = statistics.median(bm.execute(g, obs)[1].stage_ms("beamform") for _ in range(5))
+    node = g.nodes["beamform"].fn
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    alone = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        a.record()
+        node(obs)
+        b.record()
+        torch.cuda.synchronize()
+        alone.append(a.elapsed_time(b))
+    assert stage >= 0.8 * statistics.median(alone), (stage, alone)
