@@ -97,7 +97,7 @@ def synth_frames(ctx, n_s, n_frames, seed0):
     return out
 
 
-def dropin_fps(ctx, grid, host, interp, n_frames=48, warmup=4):
+def dropin_fps(ctx, grid, host, interp, n_frames=200, warmup=8):
     """Frames/s a reference user sees calling the drop-in operator chain one
     frame at a time: ``execute(build_graph(bmode_chain(...)), (RfFrame, ctx))``
     with numpy RF in and the numpy display read back (pageable H2D/D2H and a
