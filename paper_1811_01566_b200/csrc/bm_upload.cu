@@ -12,6 +12,7 @@
 // (streaming) stores, which leave the staging lines in DRAM, not dirty in
 // the CPU caches.
 #include <emmintrin.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -53,11 +54,22 @@ void stream_copy(char* d, const char* s, size_t n) {
 // A fixed pool of copy threads, woken per piece.  Workers spin briefly
 // between pieces (the next piece of a frame follows within microseconds),
 // then sleep on a condition variable.  Calls from several host threads are
-// serialised.  The pool is never destroyed (no join at process exit).
+// serialised.  The pool is never destroyed (no join at process exit); a
+// forked child (which inherits the pool but not its threads) builds its own.
 class CopyPool {
  public:
   static CopyPool& get() {
-    static CopyPool* p = new CopyPool();
+    static std::atomic<CopyPool*> pool{nullptr};
+    static std::mutex make_mu;
+    CopyPool* p = pool.load(std::memory_order_acquire);
+    if (p == nullptr || p->pid_ != getpid()) {
+      std::lock_guard<std::mutex> lk(make_mu);
+      p = pool.load(std::memory_order_acquire);
+      if (p == nullptr || p->pid_ != getpid()) {
+        p = new CopyPool();
+        pool.store(p, std::memory_order_release);
+      }
+    }
     return *p;
   }
 
@@ -82,7 +94,7 @@ class CopyPool {
   std::mutex& call_mutex() { return call_mu_; }
 
  private:
-  CopyPool() {
+  CopyPool() : pid_(getpid()) {
     const unsigned hw = std::thread::hardware_concurrency();
     nthreads_ = (int)std::max(1u, std::min(8u, hw ? hw : 1u));
     for (int i = 1; i < nthreads_; ++i) std::thread([this, i] { worker(i); }).detach();
@@ -114,6 +126,7 @@ class CopyPool {
     }
   }
 
+  const pid_t pid_;
   int nthreads_ = 1;
   std::mutex mu_, call_mu_;
   std::condition_variable cv_;

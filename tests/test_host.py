@@ -93,6 +93,18 @@ def test_invalid_arguments_rejected_without_gpu():
     assert lib.bm_analytic_signal(0, None, None, 1, 8, 1, None, 0, None) == 1
     assert lib.bm_envelope_display(0, None, None, None, None, 1, 8, 4, 30.0, None, 0, None) == 1
     assert lib.bm_display(0, None, None, None, None, 1, 4, 30.0, None) == 1
+    # host-frame upload: null / misaligned counter, decreasing piece ends,
+    # a counter without values -- all refused before any CUDA call
+    assert lib.bm_stream_write_u32(None, 1, None) == 1
+    assert lib.bm_stream_write_u32(ctypes.c_void_p(2), 1, None) == 1
+    buf = ctypes.create_string_buffer(64)
+    p = ctypes.c_void_p(ctypes.addressof(buf))
+    ends = (ctypes.c_int64 * 2)(32, 16)
+    assert lib.bm_host_upload(p, p, p, ends, 2, None, None, None) == 1
+    ends = (ctypes.c_int64 * 1)(16)
+    assert lib.bm_host_upload(p, p, p, ends, 1, p, None, None) == 1
+    assert lib.bm_host_upload(None, p, p, ends, 1, None, None, None) == 1
+    assert lib.bm_host_upload(p, p, p, ends, 0, None, None, None) == 1
     assert lib.bm_display_tiles(0, None, 2, 9, 2, 4, None, None, 30.0, None) == 1
     assert lib.bm_pad_traces(0, None, 8, 1, 8, None, 8, None) == 1
 
