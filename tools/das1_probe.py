@@ -15,7 +15,8 @@ import paper_1811_01566_b200 as bm  # noqa: E402
 from paper_1811_01566_b200 import _native as N  # noqa: E402
 
 args = [a for a in sys.argv[1:] if "=" not in a]
-for kv in (a for a in sys.argv[1:] if "=" in a):  # library tuning hooks, e.g. das_tjc=64
+write_json = "no_json=1" not in sys.argv  # the run under ncu must not overwrite it
+for kv in (a for a in sys.argv[1:] if "=" in a and a != "no_json=1"):  # tuning hooks, e.g. das_tjc=64
     k, v = kv.split("=")
     N.load().bm_debug_set(N.DEBUG_KEYS[k], int(v))
 only = args or ["cfg2", "cfg1", "cfg3", "cfg5", "sta-paper", "pwi-paper"]
@@ -47,4 +48,5 @@ ctx, grid, n_s = bm.environment.config_geometry("cfg2")
 host = bench.synth_frames(ctx, n_s, 8, 0)
 res["dropin_fps_cfg2"] = round(bench.dropin_fps(ctx, grid, host, "linear"), 1)
 print("dropin", res["dropin_fps_cfg2"])
-json.dump(res, open("gpurun_out/das1_probe.json", "w"), indent=1)
+if write_json:
+    json.dump(res, open("gpurun_out/das1_probe.json", "w"), indent=1)

@@ -26,6 +26,6 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:anal
     > gpurun_out/ncu_k2.log 2>&1; echo "k2 capture rc=$?"; summ prof_k2
 python tools/das1_probe.py > gpurun_out/das1.log 2>&1; tail -8 gpurun_out/das1.log
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:das_tma -s 3 -c 1 \
-    -o gpurun_out/prof_das1 python tools/das1_probe.py cfg2 > gpurun_out/ncu_das1.log 2>&1; echo "das1 capture rc=$?"; summ prof_das1
+    -o gpurun_out/prof_das1 python tools/das1_probe.py cfg2 no_json=1 > gpurun_out/ncu_das1.log 2>&1; echo "das1 capture rc=$?"; summ prof_das1
 python tools/k2_probe.py > gpurun_out/k2.log 2>&1; tail -4 gpurun_out/k2.log
 du -sh gpurun_out

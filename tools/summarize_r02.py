@@ -51,7 +51,17 @@ copy("bench_default.log", "r02_bench_default.jsonl")
 copy("bench_reference.log", "r02_bench_reference.jsonl")
 copy("pt_gpu.log", "r02_pytest_gpu.log")
 copy("smoke.log", "r02_smoke.log")
-copy("das1_probe.json", "r02_das_one_frame.json")
+# the one-frame numbers come from the plain das1_probe run's log (its json is
+# overwritten by the later run under ncu, whose timings are not bench values)
+if os.path.exists(os.path.join(OUT, "das1.log")):
+    one_frame = {}
+    for line in open(os.path.join(OUT, "das1.log")):
+        name, _, rest = line.strip().partition(" ")
+        if rest.startswith("{"):
+            one_frame[name] = json.loads(rest)
+        elif name == "dropin":
+            one_frame["dropin_fps_cfg2"] = float(rest)
+    json.dump(one_frame, open(os.path.join(PROF, "r02_das_one_frame.json"), "w"), indent=1)
 copy("k2_probe.json", "r02_k2_probe.json")
 
 rows = [r for r in csv.reader(open(os.path.join(OUT, "launches.csv"))) if len(r) > 5]
