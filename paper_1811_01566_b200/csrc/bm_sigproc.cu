@@ -223,17 +223,24 @@ __device__ __forceinline__ void reg_pair_hilbert(const float2* tw, int t, float2
   // (2) twiddle Wn^(t k1)
 #pragma unroll
   for (int p = 1; p < R; ++p) v[p] = c_mul(v[p], tw[t * brev_c<R>(p)]);
-  // (3) 32-point DIF across the warp: lane t then holds k2 = brev5(t)
+  // (3) 32-point DIF across the warp: lane t then holds k2 = brev5(t).
+  // Branch-free butterflies: with s = -1 on the upper lane of each pair (+1
+  // on the lower) and its twiddle w' (1 on the lower lane), both lanes
+  // compute (s v + q) w' -- the lower lane's a + b, the upper's (a - b) w --
+  // the same roundings as the two-sided form, without computing both sides
+  // and selecting (~5 instructions fewer per element and stage)
 #pragma unroll
   for (int h = 16; h >= 1; h >>= 1) {
     const bool up = (t & h) != 0;
-    const float2 w = tw[(t & (h - 1)) * (N / (2 * h))];
+    const float sg = up ? -1.0f : 1.0f;
+    const float2 w = up ? tw[(t & (h - 1)) * (N / (2 * h))] : make_float2(1.0f, 0.0f);
 #pragma unroll
     for (int p = 0; p < R; ++p) {
       float2 q;
       q.x = __shfl_xor_sync(0xffffffffu, v[p].x, h);
       q.y = __shfl_xor_sync(0xffffffffu, v[p].y, h);
-      v[p] = up ? c_mul(c_sub(q, v[p]), w) : c_add(v[p], q);
+      const float2 d = make_float2(fmaf(v[p].x, sg, q.x), fmaf(v[p].y, sg, q.y));
+      v[p] = c_mul(d, w);  // exact on the lower lane (w = 1)
     }
   }
   // (4) Hilbert rotation -i sgn(k) at k = k1 + R k2
@@ -242,18 +249,22 @@ __device__ __forceinline__ void reg_pair_hilbert(const float2* tw, int t, float2
 #pragma unroll
     for (int p = 0; p < R; ++p) v[p] = hilbert_rot(v[p], hilbert_sign(brev_c<R>(p) + R * k2, N));
   }
-  // (5) inverse 32-point DIT across the warp (bit-reversed in, natural out)
+  // (5) inverse 32-point DIT across the warp (bit-reversed in, natural out):
+  // the upper lane multiplies its own value by the twiddle BEFORE the
+  // exchange, so each lane sends u (w b on the upper lane, a on the lower)
+  // and keeps s u + q: a + w b below, a - w b above
 #pragma unroll
   for (int h = 1; h <= 16; h <<= 1) {
     const bool up = (t & h) != 0;
-    const float2 w = c_conj(tw[(t & (h - 1)) * (N / (2 * h))]);
+    const float sg = up ? -1.0f : 1.0f;
+    const float2 w = up ? c_conj(tw[(t & (h - 1)) * (N / (2 * h))]) : make_float2(1.0f, 0.0f);
 #pragma unroll
     for (int p = 0; p < R; ++p) {
+      const float2 u = c_mul(v[p], w);  // exact on the lower lane (w = 1)
       float2 q;
-      q.x = __shfl_xor_sync(0xffffffffu, v[p].x, h);
-      q.y = __shfl_xor_sync(0xffffffffu, v[p].y, h);
-      const float2 tmp = c_mul(up ? v[p] : q, w);
-      v[p] = up ? c_sub(q, tmp) : c_add(v[p], tmp);
+      q.x = __shfl_xor_sync(0xffffffffu, u.x, h);
+      q.y = __shfl_xor_sync(0xffffffffu, u.y, h);
+      v[p] = make_float2(fmaf(u.x, sg, q.x), fmaf(u.y, sg, q.y));
     }
   }
   // (6) twiddle Wn^(-t k1)
