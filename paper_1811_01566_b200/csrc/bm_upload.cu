@@ -113,7 +113,7 @@ class CopyPool {
       uint32_t g;
       int spins = 0;
       while ((g = gen_.load(std::memory_order_acquire)) == seen) {
-        if (++spins < 20000) {
+        if (++spins < 2000) {  // ~0.1 ms: the pieces of one frame, not the gap between frames
           _mm_pause();
         } else {
           std::unique_lock<std::mutex> lk(mu_);
