@@ -106,10 +106,6 @@ __global__ void __launch_bounds__(TZ * kTileX) das_kernel(const DasArgs a) {
   const T* __restrict__ t0s = reinterpret_cast<const T*>(g.t0_smp);
   T* __restrict__ outp = reinterpret_cast<T*>(a.out) + (int64_t)blockIdx.y * a.out_stride + p;
   T acc = a.accumulate && valid ? *outp : T(0);
-  if (g.tx_ready) {  // RF still being copied in: start once the launch's transmits landed
-    if (tid == 0) wait_tx_ready(g.tx_ready, g.tx_ready_base, a.e_end);
-    __syncthreads();
-  }
   for (int e = a.e_begin; e < a.e_end; ++e) {
     T txd;
     if (PW) {
@@ -182,6 +178,11 @@ __global__ void span_kernel(const bm_das_geometry g, double f_number, int32_t* s
     span[2 * p] = i0;
     span[2 * p + 1] = i1;
   }
+}
+
+// stream-ordered hold for g.tx_ready launches of the generic kernel
+__global__ void tx_wait_kernel(const uint32_t* ctr, uint32_t base, int need) {
+  wait_tx_ready(ctr, base, need);
 }
 
 template <typename T, bool PW, bool LINEAR, bool UNIFORM, bool DSMEM, int TZ = kTileZ>
@@ -299,6 +300,14 @@ extern "C" int bm_das_beamform_range(const bm_das_geometry* g, const void* rf,
     rc = bm::das_tma64_launch(*g, rf, rf_frame_stride, out, out_frame_stride, n_frames, e_begin,
                               e_end, accumulate, s);
     if (rc >= 0) return rc;
+  }
+  if (g->tx_ready) {
+    // the generic kernel reads every transmit of the range from its first
+    // CTA on: a one-warp kernel ahead of it on the stream holds it until the
+    // copy side's counter covers the range (a wait inside the kernel body --
+    // a barrier after one thread's spin -- cost the f64 nearest kernel 2x)
+    bm::tx_wait_kernel<<<1, 32, 0, s>>>(g->tx_ready, g->tx_ready_base, e_end);
+    if ((rc = bm::cuda_status()) != BM_OK) return rc;
   }
   bm::DasArgs a{*g, rf, rf_frame_stride, out, out_frame_stride, e_begin, e_end, accumulate};
   if (g->dtype == BM_F32)
