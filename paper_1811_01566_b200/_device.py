@@ -49,6 +49,9 @@ def staged_copy_into(src, dst, stream, splits=None, counter=None, values=None):
     pool["next"] ^= 1
     esz = src.element_size()
     nbytes = src.numel() * esz
+    if nbytes != dst.numel() * dst.element_size() or not dst.is_contiguous():
+        raise ValueError("staged_copy_into: destination must be contiguous and as large as "
+                         "the source")
     buf = pool["bufs"][i]
     if buf is None or buf.numel() < nbytes:
         buf = pool["bufs"][i] = torch.empty(max(nbytes, 2 * (buf.numel() if buf is not None else 0)),

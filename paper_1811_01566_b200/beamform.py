@@ -361,6 +361,11 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | Non
     from ._device import staged_copy_into
 
     data = np.ascontiguousarray(data)
+    if data.dtype != plan.dtype:
+        raise InvalidMetadata("data", f"frame dtype {data.dtype} differs from the plan's "
+                                      f"{np.dtype(plan.dtype)}")
+    if data.ndim != 3 or data.shape[0] != plan._geom.n_tx or data.shape[1] != plan.n_rx:
+        raise InvalidMetadata("data", f"frame shape {data.shape} does not match the plan")
     n_tx, n_rx, n_s = data.shape
     pieces = max(1, min(int(pieces or plan.HOST_PIECES), n_tx))
     dev = plan.device
