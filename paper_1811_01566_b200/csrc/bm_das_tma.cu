@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(128) das_table_kernel(const bm_das_geometry g,
 // the second frame reuse the first frame's addresses plus the frame-plane
 // offset of the staged box.  A pass then covers FP * FT frames (box
 // {W, G, FP * FT}); each accumulator keeps the reference's e -> j order.
+// WM (weighted kernels): the weight mode fixed at compile time -- 1 rectangular
+// with an F-number gate, 2 Hann without, 3 Hann with -- or 0, read from the
+// geometry at run time
 template <bool PW, bool LINEAR, bool T0, bool IDMAP, int TJC, bool WT = false, int FP = 1,
-          int FT = 1, int WI = 0>
+          int FT = 1, int WI = 0, int WM = 0>
 __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
     das_tma_kernel(const __grid_constant__ CUtensorMap rf_map, const TmaArgs a) {
   using O = R<float>;
@@ -328,16 +331,17 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   // pixel), else the row of each pixel's span width -- a tile's pixels use a
   // handful of rows, so they stay L1-resident
   const float* hglob = reinterpret_cast<const float*>(g.hann);
-  const bool hann = WT && g.window == BM_HANN;
+  const bool hann = WT && (WM ? WM >= 2 : g.window == BM_HANN);
+  const bool gated = WM ? WM != 2 : g.span != nullptr;  // an F-number span per pixel
   auto hann_row = [&](int i0, int i1) -> const float* {
-    const int cnt = g.span ? max(0, min(i1 - i0 + 1, n_el)) : n_el;
+    const int cnt = gated ? max(0, min(i1 - i0 + 1, n_el)) : n_el;
     return hglob + (int64_t)cnt * n_el;
   };
   const float* hrA = hann ? hann_row(i0A, i1A) : nullptr;
   const float* hrB = hann ? hann_row(i0B, i1B) : nullptr;
   // receive weights (w_A, w_B) of element m (beamform.py:84-109)
   auto weight_pair = [&](int m) -> u64 {
-    if (hann && !g.span) return L::splat(__ldg(hrA + m));
+    if (hann && !gated) return L::splat(__ldg(hrA + m));
     const bool inA = m >= i0A && m <= i1A, inB = m >= i0B && m <= i1B;
     const float wA = inA ? (hann ? __ldg(hrA + (m - i0A)) : 1.0f) : 0.0f;
     const float wB = inB ? (hann ? __ldg(hrB + (m - i0B)) : 1.0f) : 0.0f;
@@ -922,14 +926,17 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
     }
     if (W == 96 && !g.uniform && fp == 2 && !rt_w) {
       // weighted (Hann / F-number), 96-sample windows: 16 / 32-channel stages
-#define BM_TMA_WIW(J)                                                                      \
-  das_tma_kernel<false, false, false, true, J, true, 2, 4, 96>,                            \
-      das_tma_kernel<true, false, false, true, J, true, 2, 4, 96>,                         \
-      das_tma_kernel<false, true, false, true, J, true, 2, 4, 96>,                         \
-      das_tma_kernel<true, true, false, true, J, true, 2, 4, 96>
-      static const kfn table8[8] = {BM_TMA_WIW(16), BM_TMA_WIW(32)};
+      // ... with the weight mode compiled in (rectangular + F, Hann, Hann + F)
+#define BM_TMA_WIW(J, M)                                                                   \
+  das_tma_kernel<false, false, false, true, J, true, 2, 4, 96, M>,                         \
+      das_tma_kernel<true, false, false, true, J, true, 2, 4, 96, M>,                      \
+      das_tma_kernel<false, true, false, true, J, true, 2, 4, 96, M>,                      \
+      das_tma_kernel<true, true, false, true, J, true, 2, 4, 96, M>
+      static const kfn table8[24] = {BM_TMA_WIW(16, 1), BM_TMA_WIW(32, 1), BM_TMA_WIW(16, 2),
+                                     BM_TMA_WIW(32, 2), BM_TMA_WIW(16, 3), BM_TMA_WIW(32, 3)};
 #undef BM_TMA_WIW
-      k = table8[(tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
+      const int wm = g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
+      k = table8[(wm - 1) * 8 + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
     }
   }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

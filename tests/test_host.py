@@ -230,8 +230,9 @@ def test_no_contracted_fma_in_das_kernels():
     # + 16 of them weighted (Hann / F-number)
     # + 32 uniform four-frames-per-thread 16ch tma with a compile-time window
     #   (96 / 128 / 160 / 192 samples) x FP = 1 / 2 x {STA, PW} x {nearest, linear}
-    # + 8 weighted FP = 2 ones with a 96-sample compile-time window, 16 / 32ch
-    assert len(das) == 190
+    # + 24 weighted FP = 2 ones with a 96-sample compile-time window, 16 / 32ch,
+    #   with the weight mode compiled in (rectangular + F, Hann, Hann + F)
+    assert len(das) == 206
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
