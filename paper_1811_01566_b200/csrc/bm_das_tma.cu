@@ -339,8 +339,20 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   };
   const float* hrA = hann ? hann_row(i0A, i1A) : nullptr;
   const float* hrB = hann ? hann_row(i0B, i1B) : nullptr;
+  // WM = 3: the Hann rows zero-padded by n_el on both sides (g.hann_pad), so
+  // a pixel's weight of element m is one read at m - i0 + n_el, zero outside
+  // its span -- no span tests or selects per channel
+  const float* hpA = nullptr;
+  const float* hpB = nullptr;
+  if (WM == 3) {
+    const float* hp = reinterpret_cast<const float*>(g.hann_pad);
+    const int cA = max(0, min(i1A - i0A + 1, n_el)), cB = max(0, min(i1B - i0B + 1, n_el));
+    hpA = hp + (int64_t)cA * 3 * n_el + n_el - i0A;
+    hpB = hp + (int64_t)cB * 3 * n_el + n_el - i0B;
+  }
   // receive weights (w_A, w_B) of element m (beamform.py:84-109)
   auto weight_pair = [&](int m) -> u64 {
+    if (WM == 3) return L::make(__ldg(hpA + m), __ldg(hpB + m));
     if (hann && !gated) return L::splat(__ldg(hrA + m));
     const bool inA = m >= i0A && m <= i1A, inB = m >= i0B && m <= i1B;
     const float wA = inA ? (hann ? __ldg(hrA + (m - i0A)) : 1.0f) : 0.0f;
@@ -935,8 +947,10 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
       static const kfn table8[24] = {BM_TMA_WIW(16, 1), BM_TMA_WIW(32, 1), BM_TMA_WIW(16, 2),
                                      BM_TMA_WIW(32, 2), BM_TMA_WIW(16, 3), BM_TMA_WIW(32, 3)};
 #undef BM_TMA_WIW
+      // (Hann + F needs the padded rows; without them the run-time kernel stays)
       const int wm = g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
-      k = table8[(wm - 1) * 8 + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
+      if (wm != 3 || g.hann_pad)
+        k = table8[(wm - 1) * 8 + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
     }
   }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
