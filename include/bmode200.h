@@ -121,12 +121,12 @@ typedef struct bm_das_geometry {
                                 copy side advancing it behind each landed transmit
                                 group with bm_stream_write_u32.  NULL = RF resident */
   uint32_t tx_ready_base;
-  const float* hann_pad;     /* optional DEVICE table (f32 Hann + F-number plans): the
+  const float* weight_pad;   /* optional DEVICE table (f32 Hann + F-number plans): the
                                 `hann` rows zero-padded by n_elements on both sides,
                                 [n_elements + 1][3 n_elements]; the TMA kernel then
                                 reads a pixel's weight of element m at row (span
                                 width), column m - i0 + n_elements, without span
-                                tests.  NULL = the tests and `hann` */
+                                tests.  NULL = the span tests and `hann` */
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64

@@ -49,7 +49,7 @@ class DasGeometry(ctypes.Structure):
         ("rx_map", ctypes.c_void_p), ("t0_smp", ctypes.c_void_p), ("hann", ctypes.c_void_p),
         ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32), ("tile_ls", ctypes.c_int32),
         ("rx_table", ctypes.c_void_p), ("tx_ready", ctypes.c_void_p),
-        ("tx_ready_base", ctypes.c_uint32), ("hann_pad", ctypes.c_void_p),
+        ("tx_ready_base", ctypes.c_uint32), ("weight_pad", ctypes.c_void_p),
     ]
 
 

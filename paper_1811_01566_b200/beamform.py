@@ -120,11 +120,12 @@ class DasPlan:
         if apod.window == "hann":
             tab = hann_weight_table(ctx.n_elements).astype(dtype)
             self._bufs["hann"] = dev_t(tab)
-            if apod.f_number > 0.0 and np.dtype(dtype) == np.float32:
-                n_el = ctx.n_elements  # zero-padded rows for the TMA kernel (g.hann_pad)
-                pad = np.zeros((n_el + 1, 3 * n_el), dtype=tab.dtype)
-                pad[:, n_el:2 * n_el] = tab
-                self._bufs["hann_pad"] = dev_t(pad)
+        if apod.window == "hann" and apod.f_number > 0.0 and np.dtype(dtype) == np.float32:
+            # the Hann rows zero-padded on both sides for the TMA kernel (g.weight_pad)
+            n_el = ctx.n_elements
+            pad = np.zeros((n_el + 1, 3 * n_el), dtype=dtype)
+            pad[:, n_el:2 * n_el] = tab
+            self._bufs["weight_pad"] = dev_t(pad)
         self.uniform = apod.window == "rectangular" and apod.f_number == 0.0
 
         g = N.DasGeometry()

@@ -53,7 +53,7 @@ def test_geometry_struct_layout():
     assert N.DasGeometry.rx_table.offset == 16 * 4 + 2 * 8 + 10 * 8 + 8
     assert N.DasGeometry.tx_ready.offset == 16 * 4 + 2 * 8 + 10 * 8 + 16
     assert N.DasGeometry.tx_ready_base.offset == 16 * 4 + 2 * 8 + 10 * 8 + 24
-    assert N.DasGeometry.hann_pad.offset == 16 * 4 + 2 * 8 + 10 * 8 + 32
+    assert N.DasGeometry.weight_pad.offset == 16 * 4 + 2 * 8 + 10 * 8 + 32
     assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 40
 
 
