@@ -201,14 +201,18 @@ def envelope_peak_device(x, n_frames: int, n_z: int, n_x: int):
     return env, peak
 
 
-def _dyn_device(e, range_db: float, peak=None):
-    """dB mapping on the device in e's precision; returns (disp, status)."""
+def _dyn_device(e, range_db: float, peak=None, disp=None, status=None):
+    """dB mapping on the device in e's precision; returns (disp, status).
+    ``disp`` / ``status`` may be given, e.g. pinned host tensors the kernel
+    then writes over the bus (no separate device-to-host copy)."""
     import torch
 
     dev = e.device
     code = N.BM_F32 if e.dtype == torch.float32 else N.BM_F64
-    disp = torch.empty_like(e)
-    status = torch.empty(1, dtype=torch.int32, device=dev)
+    if disp is None:
+        disp = torch.empty_like(e)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=dev)
     with N.on_device(dev):
         if peak is None:
             peak = torch.empty(1, dtype=torch.int32 if code == N.BM_F32 else torch.int64, device=dev)
