@@ -354,7 +354,8 @@ def _copy_state(dev):
     return st
 
 
-def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | None = None):
+def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | None = None,
+                  out=None):
     """One HOST frame (numpy, [n_tx, n_rx, n_s]) -> device rf image, the
     frame's host->device copy overlapping its own Delay-and-Sum (SURVEY
     8(f) #1): the copy runs on a copy stream in ``pieces`` transmit groups,
@@ -362,7 +363,9 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | Non
     (bm_stream_write_u32), and ONE launch -- issued once every piece is
     enqueued, so no exception can strand it -- reads transmit e as soon as
     the count passes it (g.tx_ready).  The launch is the same kernel over
-    the same data, so the bits equal a launch on the resident frame."""
+    the same data, so the bits equal a launch on the resident frame.
+    ``out``: optional [1, n_z, n_x] destination, e.g. pinned host memory the
+    kernel then writes over the bus."""
     import torch
 
     from ._device import staged_copy_into
@@ -381,7 +384,8 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | Non
     # a buffer per call (plans are shared between threads); the copy stream
     # writes it only after the allocating stream's earlier work
     rf = torch.empty((1, n_tx, n_rx, n_s), dtype=plan.torch_dtype, device=dev)
-    out = torch.empty((1,) + plan.shape, dtype=plan.torch_dtype, device=dev)
+    if out is None:
+        out = torch.empty((1,) + plan.shape, dtype=plan.torch_dtype, device=dev)
     cs.wait_stream(comp)
     base = st["base"]
     st["base"] = (base + n_tx) & 0xFFFFFFFF
@@ -408,9 +412,15 @@ def das_beamform(frame: RfFrame, ctx, grid, apod: ApodizationSpec = ApodizationS
         plan = DasPlan(ctx, grid, apod, dtype, frame.n_rx)
     host = not _is_torch(frame.data)
     if host and plan.host_overlap_ok(frame.n_samples):
-        img = beamform_host(plan, frame.data, interp)  # copy/DAS overlap by transmit chunk
-    else:
-        img = plan.beamform_batch(to_device(frame.data, plan.device), interp)
+        import torch
+
+        # the upload overlaps the DAS, which writes the image straight into
+        # pinned host memory (numpy in -> numpy out, no device-to-host copy)
+        out = torch.empty((1,) + plan.shape, dtype=plan.torch_dtype, pin_memory=True)
+        beamform_host(plan, frame.data, interp, out=out)
+        torch.cuda.current_stream(plan.device).synchronize()
+        return BmodeImage(out[0].numpy(), stage="rf", grid=grid)
+    img = plan.beamform_batch(to_device(frame.data, plan.device), interp)
     return BmodeImage(img.cpu().numpy() if host else img, stage="rf", grid=grid)
 
 
