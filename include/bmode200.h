@@ -127,6 +127,12 @@ typedef struct bm_das_geometry {
                                 reads a pixel's weight of element m at row (span
                                 width), column m - i0 + n_elements, without span
                                 tests.  NULL = the span tests and `hann` */
+  int32_t tile_ls_nearest;   /* set by bm_das_prepare (contiguous maps): the tile shape
+                                for nearest-interpolation launches without a delay
+                                table when its staged window is smaller than
+                                tile_ls's (more pipeline stages pay for nearest's
+                                lighter gathers); 0 = tile_ls */
+  int32_t window_hint_g4_nearest; /* its 4-channel window bound */
 } bm_das_geometry;
 
 /* Per-pixel dynamic-aperture span |x_elem - x| <= z / (2 F), in f64

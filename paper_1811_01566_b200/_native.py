@@ -50,6 +50,7 @@ class DasGeometry(ctypes.Structure):
         ("span", ctypes.c_void_p), ("rx_contig", ctypes.c_int32), ("tile_ls", ctypes.c_int32),
         ("rx_table", ctypes.c_void_p), ("tx_ready", ctypes.c_void_p),
         ("tx_ready_base", ctypes.c_uint32), ("weight_pad", ctypes.c_void_p),
+        ("tile_ls_nearest", ctypes.c_int32), ("window_hint_g4_nearest", ctypes.c_int32),
     ]
 
 

@@ -104,6 +104,8 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->rx_identity = 0;
   g->rx_contig = 0;
   g->tile_ls = 3;
+  g->tile_ls_nearest = 0;
+  g->window_hint_g4_nearest = 0;
   if (g->n_z < 1 || g->n_x < 1 || g->n_elements < 1 || g->n_tx < 1) return BM_ERR_INVALID_ARGUMENT;
   // window bound of a tz x tx-pixel tile: tx delay range + rx delay range
   // (each <= k * tile diagonal) + margins
@@ -173,19 +175,31 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   // 64 x 4 tiles W 96 vs 192, 0.77 -> 0.53 ms/frame; cfg1 8 x 32 W 128 vs 152
   // is 2 % slower)
   int ls = 3, wbest = g->n_elements >= 4 ? g4_for(3) : 0;
+  int ls_near = 0, w_near = 0;
   if (contig && g->n_elements >= 4) {
     const int force = bm::debug_override(BM_DBG_DAS_TILE);  // override: 1 (64 x 4) .. 4 (8 x 32)
     if (force >= 1 && force <= 4) {
       ls = force;
       wbest = g4_for(ls);
     } else {
+      int wc[5] = {0, 0, 0, wbest, 0};
       for (int c : {1, 2, 4}) {
-        const int w = g4_for(c);
+        const int w = wc[c] = g4_for(c);
         if (w * 5 <= wbest * 4 && w < wbest) {
           ls = c;
           wbest = w;
         }
       }
+      // nearest interpolation gathers one sample per contribution: a smaller
+      // window (more stages) pays at any margin (cfg1: 8 x 32 tiles, W 128 vs
+      // 152: 0.65 vs 0.59 of the gather roof; linear 3 % slower there)
+      w_near = wbest;
+      for (int c : {1, 2, 3, 4})
+        if (wc[c] > 0 && wc[c] < w_near) {
+          ls_near = c;
+          w_near = wc[c];
+        }
+      if (ls_near == ls) ls_near = 0;
     }
   }
   g->tile_ls = ls;
@@ -194,5 +208,9 @@ extern "C" int bm_das_prepare(bm_das_geometry* g, const double* elem_x, const do
   g->window_hint = W;
   g->window_hint_wide = W_wide;
   if (g->n_elements >= 4) g->window_hint_g4 = wbest;
+  if (ls_near) {
+    g->tile_ls_nearest = ls_near;
+    g->window_hint_g4_nearest = w_near;
+  }
   return BM_OK;
 }

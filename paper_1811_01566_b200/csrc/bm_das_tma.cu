@@ -669,9 +669,17 @@ EncodeTiledFn encode_tiled() {
 
 // row stride of the staged windows: one channel per box (128-B aligned rows)
 // or 4 adjacent channels per box sharing one window start
+// nearest-interpolation launches without a delay table may take their own
+// tile shape (bm_das_prepare: tile_ls_nearest)
+static bool tma_nearest_tile(const bm_das_geometry& g) {
+  return g.interp == BM_NEAREST && !g.rx_table && g.rx_contig && g.tile_ls_nearest >= 1 &&
+         g.tile_ls_nearest <= 4 && g.window_hint_g4_nearest > 0;
+}
+
 int tma_window(const bm_das_geometry& g) {
-  const int w =
-      g.rx_contig && g.window_hint_g4 > 0 ? g.window_hint_g4 : (g.window_hint + 31) & ~31;
+  const int w = tma_nearest_tile(g) ? g.window_hint_g4_nearest
+                : g.rx_contig && g.window_hint_g4 > 0 ? g.window_hint_g4
+                                                      : (g.window_hint + 31) & ~31;
   // within 8 samples below a multiple of 32 (up to 192): round up, so a
   // kernel with a compile-time window (WI = 96 .. 192) covers it; larger
   // roundings would cost stages of shared memory
@@ -682,6 +690,7 @@ int tma_window(const bm_das_geometry& g) {
 // tile shape of a launch: contiguous maps use the prepared shape, other maps
 // the 16 x 16 tiles window_hint bounds
 int tma_ls(const bm_das_geometry& g) {
+  if (tma_nearest_tile(g)) return g.tile_ls_nearest;
   return g.rx_contig && g.tile_ls >= 1 && g.tile_ls <= 4 ? g.tile_ls : 3;
 }
 int tma_tiles(const bm_das_geometry& g) {

@@ -54,7 +54,8 @@ def test_geometry_struct_layout():
     assert N.DasGeometry.tx_ready.offset == 16 * 4 + 2 * 8 + 10 * 8 + 16
     assert N.DasGeometry.tx_ready_base.offset == 16 * 4 + 2 * 8 + 10 * 8 + 24
     assert N.DasGeometry.weight_pad.offset == 16 * 4 + 2 * 8 + 10 * 8 + 32
-    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 40
+    assert N.DasGeometry.tile_ls_nearest.offset == 16 * 4 + 2 * 8 + 10 * 8 + 40
+    assert ctypes.sizeof(N.DasGeometry) == 16 * 4 + 2 * 8 + 10 * 8 + 48
 
 
 def test_debug_keys_match_header_enum():
