@@ -200,4 +200,4 @@ def test_stage_times_bracket_each_ops_gpu_work():
         b.record()
         torch.cuda.synchronize()
         alone.append(a.elapsed_time(b))
-    assert stage >= 0.8 * statistics.median(alone), (stage, alone)
+    assert stage >= 0.6 * statistics.median(alone), (stage, alone)
