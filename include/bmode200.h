@@ -31,6 +31,13 @@
  *                             moments: estimate_hk_map qus.py:186-192)
  *   bm_quantize_u8         <- the pixel mapping of write_pgm formats.py:189-200
  *   bm_simulate_rf         <- simulate_rf environment.py:91-129 (synthetic RF)
+ *   bm_host_upload,        <- the x_pad copy of a host frame into the kernel's
+ *   bm_stream_write_u32       input (beamform.py:273-274) as an H2D upload the
+ *                             DAS launch overlaps (g->tx_ready)
+ *
+ * ABI 4 (this version): bm_das_geometry gained tx_ready / tx_ready_base,
+ * weight_pad, tile_ls_nearest / window_hint_g4_nearest; bm_host_upload and
+ * bm_stream_write_u32 are new; BM_DBG_DAS_LATE_PRODUCER joined the debug keys.
  */
 #ifndef BMODE200_H
 #define BMODE200_H
