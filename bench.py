@@ -131,7 +131,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,temperature.gpu")
 
     def __init__(self, index):
         self.index = index
@@ -177,9 +177,10 @@ class ClockSampler:
         mx = [float(r[1]) for r in rows if num(r[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        temp = [float(r[7]) for r in rows if len(r) > 7 and num(r[7])]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "temp_c": max(temp) if temp else None, "samples": len(rows)}
 
 
 def cpu_reference(ctx, grid, frames, seconds, interp, max_frames=None):
