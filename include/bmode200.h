@@ -4,7 +4,10 @@
  * Every entry point is stream-ordered, stateless and re-entrant: it enqueues
  * work on `stream` (a cudaStream_t passed as void*; NULL = legacy default
  * stream) and returns immediately.  No entry point allocates memory; all
- * buffers are caller-owned DEVICE pointers.  Inputs are never written.
+ * buffers are caller-owned and device-accessible (device memory, or pinned
+ * host memory a kernel may write over the bus -- the display of a host-origin
+ * chain); bm_host_upload alone reads a pageable host frame.  Inputs are never
+ * written.
  * Return value: BM_OK (0) or a BM_ERR_* code (see bm_error_string()).
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/echopipe):
