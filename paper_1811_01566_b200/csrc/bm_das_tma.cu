@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(32 * (4 * FP + 1), 2)
   // the tile's active spans has weight 0 for all its pixels, so its terms
   // are exact zeros (x is finite, acc never -0: acc + (+-0) == acc) and the
   // stages of channels outside it are neither loaded nor computed
-  constexpr bool SKIP = WT && IDMAP;
+  // (no F-number gate, WM = 2: nothing to skip -- the skip code is compiled out)
+  constexpr bool SKIP = WT && IDMAP && WM != 2;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == NCW;
@@ -879,6 +880,25 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   if (tjc == 128) {
     if (!tma_has128(g)) return -1;
     k = pw ? das_tma_kernel<true, true, false, true, 128> : das_tma_kernel<false, true, false, true, 128>;
+  }
+  if (!g.uniform && fp == 1 && ft == 1 && g.rx_contig && !g.t0_nonzero && (tjc == 32 || tjc == 64)) {
+    // one-frame weighted launches (the drop-in path with Hann / F-number
+    // receive weights): the weight mode compiled in, as for the batched
+    // kernels -- the run-time form is 2.2x the uniform kernel's time there
+    // (branches, span tests, and an instruction footprint that misses the
+    // instruction cache)
+    const int wm = g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
+    if (wm != 3 || g.weight_pad) {
+#define BM_TMA_W1(J, M)                                                                    \
+  das_tma_kernel<false, false, false, true, J, true, 1, 1, 0, M>,                          \
+      das_tma_kernel<true, false, false, true, J, true, 1, 1, 0, M>,                       \
+      das_tma_kernel<false, true, false, true, J, true, 1, 1, 0, M>,                       \
+      das_tma_kernel<true, true, false, true, J, true, 1, 1, 0, M>
+      static const kfn table9[24] = {BM_TMA_W1(32, 1), BM_TMA_W1(64, 1), BM_TMA_W1(32, 2),
+                                     BM_TMA_W1(64, 2), BM_TMA_W1(32, 3), BM_TMA_W1(64, 3)};
+#undef BM_TMA_W1
+      k = table9[(wm - 1) * 8 + (tjc == 64 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];
+    }
   }
   if (fp == 2) {
 #define BM_TMA_FP2(J, WT)                                                                   \

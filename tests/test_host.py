@@ -234,7 +234,9 @@ def test_no_contracted_fma_in_das_kernels():
     #   (96 / 128 / 160 / 192 samples) x FP = 1 / 2 x {STA, PW} x {nearest, linear}
     # + 24 weighted FP = 2 ones with a 96-sample compile-time window, 16 / 32ch,
     #   with the weight mode compiled in (rectangular + F, Hann, Hann + F)
-    assert len(das) == 206
+    # + 24 one-frame weighted ones (FP = FT = 1, 32 / 64ch, contiguous maps, no
+    #   t0) with the weight mode compiled in
+    assert len(das) == 230
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
