@@ -938,18 +938,26 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
   if (ft == 4) {
     // four frames per thread, contiguous maps, no t0, uniform and weighted;
     // rows: uniform / weighted x FP = 1 / 2 x 16 / 32-channel stages
-#define BM_TMA_FT4(J, F, WT)                                                               \
-  das_tma_kernel<false, false, false, true, J, WT, F, 4>,                                  \
-      das_tma_kernel<true, false, false, true, J, WT, F, 4>,                               \
-      das_tma_kernel<false, true, false, true, J, WT, F, 4>,                               \
-      das_tma_kernel<true, true, false, true, J, WT, F, 4>
-    static const kfn table4[32] = {
-        BM_TMA_FT4(16, 1, false), BM_TMA_FT4(32, 1, false), BM_TMA_FT4(16, 2, false),
-        BM_TMA_FT4(32, 2, false), BM_TMA_FT4(16, 1, true),  BM_TMA_FT4(32, 1, true),
-        BM_TMA_FT4(16, 2, true),  BM_TMA_FT4(32, 2, true)};
+    // (weighted: the weight mode compiled in -- rectangular + F, Hann, Hann
+    // + F over g.weight_pad; without the padded rows Hann + F takes the
+    // generic kernel)
+#define BM_TMA_FT4(J, F, WT, M)                                                            \
+  das_tma_kernel<false, false, false, true, J, WT, F, 4, 0, M>,                            \
+      das_tma_kernel<true, false, false, true, J, WT, F, 4, 0, M>,                         \
+      das_tma_kernel<false, true, false, true, J, WT, F, 4, 0, M>,                         \
+      das_tma_kernel<true, true, false, true, J, WT, F, 4, 0, M>
+#define BM_TMA_FT4W(M)                                                                     \
+  BM_TMA_FT4(16, 1, true, M), BM_TMA_FT4(32, 1, true, M), BM_TMA_FT4(16, 2, true, M),      \
+      BM_TMA_FT4(32, 2, true, M)
+    static const kfn table4[64] = {
+        BM_TMA_FT4(16, 1, false, 0), BM_TMA_FT4(32, 1, false, 0), BM_TMA_FT4(16, 2, false, 0),
+        BM_TMA_FT4(32, 2, false, 0), BM_TMA_FT4W(1), BM_TMA_FT4W(2), BM_TMA_FT4W(3)};
+#undef BM_TMA_FT4W
 #undef BM_TMA_FT4
     if (tjc > 32) return -1;
-    k = table4[(g.uniform ? 0 : 16) + (fp == 2 ? 8 : 0) + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) +
+    const int wm4 = g.uniform ? 0 : g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
+    if (wm4 == 3 && !g.weight_pad) return -1;
+    k = table4[wm4 * 16 + (fp == 2 ? 8 : 0) + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) +
                (pw ? 1 : 0)];
     // compile-time window widths for the uniform 16-channel kernels: the
     // frame-plane offsets of frames 1..3 become LDS immediates (cfg2: 12 %
@@ -979,7 +987,7 @@ int das_tma_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride, 
       static const kfn table8[24] = {BM_TMA_WIW(16, 1), BM_TMA_WIW(32, 1), BM_TMA_WIW(16, 2),
                                      BM_TMA_WIW(32, 2), BM_TMA_WIW(16, 3), BM_TMA_WIW(32, 3)};
 #undef BM_TMA_WIW
-      // (Hann + F needs the padded rows; without them the run-time kernel stays)
+      // (Hann + F without the padded rows already left for the generic kernel)
       const int wm = g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
       if (wm != 3 || g.weight_pad)
         k = table8[(wm - 1) * 8 + (tjc == 32 ? 4 : 0) + (lin ? 2 : 0) + (pw ? 1 : 0)];

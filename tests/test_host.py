@@ -229,14 +229,15 @@ def test_no_contracted_fma_in_das_kernels():
     # + 20 two-frames-per-thread tma (uniform identity map, no t0) x {STA, PW} x
     # {nearest, linear}: FP = 1 x {32, 64}ch, FP = 2 x {16, 32, 64}ch
     # + 16 four-frames-per-thread tma, same apertures, FP = 1 / 2 x {16, 32}ch
-    # + 16 of them weighted (Hann / F-number)
+    # + 48 of them weighted, the weight mode compiled in (rectangular + F,
+    #   Hann, Hann + F)
     # + 32 uniform four-frames-per-thread 16ch tma with a compile-time window
     #   (96 / 128 / 160 / 192 samples) x FP = 1 / 2 x {STA, PW} x {nearest, linear}
     # + 24 weighted FP = 2 ones with a 96-sample compile-time window, 16 / 32ch,
     #   with the weight mode compiled in (rectangular + F, Hann, Hann + F)
     # + 24 one-frame weighted ones (FP = FT = 1, 32 / 64ch, contiguous maps, no
     #   t0) with the weight mode compiled in
-    assert len(das) == 230
+    assert len(das) == 262
     for n, lines in das.items():
         for l in lines:
             if "FFMA2" in l:
