@@ -92,13 +92,17 @@ int das_table64_build(const bm_das_geometry& g, double* table, cudaStream_t s) {
   return cuda_status();
 }
 
-template <bool PW, bool LINEAR, bool T0, bool IDMAP, bool WT>
+// WM (weighted kernels): the weight mode compiled in -- 1 rectangular with an
+// F-number gate, 2 Hann without, 3 Hann with -- or 0, read at run time (as in
+// the f32 kernel: the run-time form costs branches and instruction-cache
+// misses on every channel)
+template <bool PW, bool LINEAR, bool T0, bool IDMAP, bool WT, int WM = 0>
 __global__ void __launch_bounds__(288, 1)
     das_tma64_kernel(const __grid_constant__ CUtensorMap rf_map, const Tma64Args a) {
   using O = R<double>;
   constexpr int NTH = 288, NCW = 8, NC = 256;  // threads, consumer warps, consumer threads
   constexpr int G = IDMAP ? 4 : 1;           // traces per TMA box
-  constexpr bool SKIP = WT && IDMAP;
+  constexpr bool SKIP = WT && IDMAP && WM != 2;  // nothing to skip without an F-number
   const bm_das_geometry& g = a.g;
   const int n_el = g.n_elements, n_tx = g.n_tx, n_rx = g.n_rx;
   const int W = a.W, nst = a.nst;
@@ -234,11 +238,12 @@ __global__ void __launch_bounds__(288, 1)
   __syncthreads();
 
   const double* hglob = reinterpret_cast<const double*>(g.hann);
-  const bool hann = WT && g.window == BM_HANN;
+  const bool hann = WT && (WM ? WM >= 2 : g.window == BM_HANN);
+  const bool gated = WM ? WM != 2 : g.span != nullptr;
   const double* hrow =
-      hann ? hglob + (int64_t)(g.span ? max(0, min(i1 - i0 + 1, n_el)) : n_el) * n_el : nullptr;
+      hann ? hglob + (int64_t)(gated ? max(0, min(i1 - i0 + 1, n_el)) : n_el) * n_el : nullptr;
   auto weight = [&](int m) -> double {
-    if (hann && !g.span) return __ldg(hrow + m);
+    if (hann && !gated) return __ldg(hrow + m);
     if (m < i0 || m > i1) return 0.0;
     return hann ? __ldg(hrow + (m - i0)) : 1.0;
   };
@@ -513,9 +518,20 @@ int das_tma64_launch(const bm_das_geometry& g, const void* rf, int64_t rf_stride
       das_tma64_kernel<true, true, true, false, WT>, das_tma64_kernel<true, true, true, true, WT>
   static const kfn table[32] = {BM_T64(false), BM_T64(true)};
 #undef BM_T64
-  const kfn k = table[(g.uniform ? 0 : 16) + (g.scheme == BM_PW ? 8 : 0) +
-                      (g.interp == BM_LINEAR ? 4 : 0) + (g.t0_nonzero ? 2 : 0) +
-                      (g.rx_contig ? 1 : 0)];
+  kfn k = table[(g.uniform ? 0 : 16) + (g.scheme == BM_PW ? 8 : 0) +
+                (g.interp == BM_LINEAR ? 4 : 0) + (g.t0_nonzero ? 2 : 0) + (g.rx_contig ? 1 : 0)];
+  if (!g.uniform && g.rx_contig && !g.t0_nonzero) {
+    // weighted, contiguous maps, no t0: the weight mode compiled in
+#define BM_T64W(M)                                                                          \
+  das_tma64_kernel<false, false, false, true, true, M>,                                     \
+      das_tma64_kernel<false, true, false, true, true, M>,                                  \
+      das_tma64_kernel<true, false, false, true, true, M>,                                  \
+      das_tma64_kernel<true, true, false, true, true, M>
+    static const kfn tablew[12] = {BM_T64W(1), BM_T64W(2), BM_T64W(3)};
+#undef BM_T64W
+    const int wm = g.window == BM_HANN ? (g.span ? 3 : 2) : 1;
+    k = tablew[(wm - 1) * 4 + (g.scheme == BM_PW ? 2 : 0) + (g.interp == BM_LINEAR ? 1 : 0)];
+  }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return BM_ERR_CUDA;
