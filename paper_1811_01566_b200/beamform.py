@@ -380,7 +380,7 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | Non
     pieces = max(1, min(int(pieces or plan.HOST_PIECES), n_tx))
     dev = plan.device
     st = _copy_state(dev)
-    cs, comp = st["stream"], torch.cuda.current_stream(dev)
+    cs, comp = st["stream"], N.current_stream(dev)
     # a buffer per call (plans are shared between threads); the copy stream
     # writes it only after the allocating stream's earlier work
     rf = torch.empty((1, n_tx, n_rx, n_s), dtype=plan.torch_dtype, device=dev)
@@ -418,7 +418,7 @@ def das_beamform(frame: RfFrame, ctx, grid, apod: ApodizationSpec = ApodizationS
         # pinned host memory (numpy in -> numpy out, no device-to-host copy)
         out = torch.empty((1,) + plan.shape, dtype=plan.torch_dtype, pin_memory=True)
         beamform_host(plan, frame.data, interp, out=out)
-        torch.cuda.current_stream(plan.device).synchronize()
+        N.current_stream(plan.device).synchronize()
         return BmodeImage(out[0].numpy(), stage="rf", grid=grid)
     img = plan.beamform_batch(to_device(frame.data, plan.device), interp)
     return BmodeImage(img.cpu().numpy() if host else img, stage="rf", grid=grid)
