@@ -23,8 +23,10 @@ def _staged_h2d(src, device):
     pinned staging buffers; the copy is enqueued on the current stream."""
     import torch
 
+    from . import _native as N
+
     out = torch.empty(src.shape, dtype=src.dtype, device=device)
-    staged_copy_into(src, out, torch.cuda.current_stream(device))
+    staged_copy_into(src, out, N.current_stream(device))
     return out
 
 
