@@ -31,7 +31,7 @@ def _staged_h2d(src, device):
 
 
 def staged_copy_into(src, dst, stream, splits=None, counter=None, values=None):
-    """Copy a contiguous CPU tensor into the device tensor ``dst`` (same
+    """Copy a CPU tensor or numpy array into the device tensor ``dst`` (same
     numel) through one of two per-thread pinned staging buffers, enqueued on
     ``stream`` by bm_host_upload (multi-threaded streaming-store host copy,
     then the DMA, piece by piece); returns the event that follows the last
@@ -49,8 +49,13 @@ def staged_copy_into(src, dst, stream, splits=None, counter=None, values=None):
         pool = _stage.pool = {"bufs": [None, None], "events": [None, None], "next": 0}
     i = pool["next"]
     pool["next"] ^= 1
-    esz = src.element_size()
-    nbytes = src.numel() * esz
+    if isinstance(src, np.ndarray):  # read straight from the array (no torch view)
+        src = np.ascontiguousarray(src)
+        esz, n, src_ptr = src.itemsize, src.size, src.ctypes.data
+    else:
+        src = src.contiguous()
+        esz, n, src_ptr = src.element_size(), src.numel(), src.data_ptr()
+    nbytes = n * esz
     if nbytes != dst.numel() * dst.element_size() or not dst.is_contiguous():
         raise ValueError("staged_copy_into: destination must be contiguous and as large as "
                          "the source")
@@ -62,15 +67,13 @@ def staged_copy_into(src, dst, stream, splits=None, counter=None, values=None):
     ev = pool["events"][i]
     if ev is not None:
         ev.synchronize()  # the DMA that last read this buffer has finished
-    n = src.numel()
     if splits is None:
         step = max(1, -(-n // 4)) if nbytes >= (4 << 20) else n
         splits = list(range(step, n, step)) + [n]
     k = len(splits)
     ends = (ctypes.c_int64 * k)(*[int(e) * esz for e in splits])
     vals = (ctypes.c_uint32 * k)(*[int(v) & 0xFFFFFFFF for v in values]) if counter else None
-    src = src.contiguous()
-    N.call("bm_host_upload", dst.data_ptr(), src.data_ptr(), buf.data_ptr(), ends, k,
+    N.call("bm_host_upload", dst.data_ptr(), src_ptr, buf.data_ptr(), ends, k,
            counter, vals, int(stream.cuda_stream))
     ev = torch.cuda.Event()
     ev.record(stream)

@@ -391,7 +391,7 @@ def beamform_host(plan: DasPlan, data, interp: str = "linear", pieces: int | Non
     st["base"] = (base + n_tx) & 0xFFFFFFFF
     ctr = st["counter"].data_ptr()
     bounds = list(_tx_chunks(n_tx, pieces))
-    done = staged_copy_into(torch.from_numpy(data), rf, cs,
+    done = staged_copy_into(data, rf, cs,
                             splits=[e1 * n_rx * n_s for _, e1 in bounds], counter=ctr,
                             values=[base + e1 for _, e1 in bounds])
     plan.beamform_batch(rf, interp, out=out, stream=comp, tx_ready=(ctr, base))
