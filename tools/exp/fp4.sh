@@ -1,3 +1,5 @@
+# pwi-paper with four warp groups per delay table (FP = 4) -- run against the
+# experimental FP = 4 build (since reverted: no gain)
 one() {
   l=$1; shift
   timeout 300 python bench.py --steps 10 --no-cpu --no-stai --no-e2e "$@" 2>/dev/null | tail -1 |
